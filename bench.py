@@ -1,0 +1,467 @@
+#!/usr/bin/env python
+"""Benchmark: DoF-updates/s of the ADER-DG hot path on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+
+One "step" is one ADER-DG time step (admissible-dt reduction, space-time
+predictor, Riemann + corrector) of the configuration over its whole mesh,
+state resident in HBM.  The headline workload is BASELINE.json configs[1]
+(config 2: 2-D Euler, 243^2 cells, p = 5, CFL 0.9/(2p+1)), whose state plus
+predictor buffers (~300 MB) exceed the 126 MB L2, so no flush is needed
+between steps.  Under torchrun (N > 1) every rank runs an independent replica
+(the path does not shard in this tier: "replicas only"); the
+value is the aggregate over ranks, timed as the max over ranks.
+
+--impl reference times the reference algorithm's own CPU implementation (the
+per-cell numpy port in oracle/, since the Python reference cannot travel to
+the GPU box) on the host cores, on a bounded sample of cells per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_1806_07984_b200 import configs as cf  # noqa: E402
+from paper_1806_07984_b200 import costs  # noqa: E402
+
+METRIC = "DoF-updates/s per time step on 1 B200; % of FP64/HBM roofline per kernel"
+UNIT = "DoF-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=47)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(cf.CONFIGS))
+    ap.add_argument("--cfl", type=float, default=None, help="override the config's CFL safety")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ ranks --
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def dist_init(ws, backend):
+    if ws > 1:
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            dist.init_process_group(backend)
+        return dist
+    return None
+
+
+def max_over_ranks(dist, x, device):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------- workloads --
+
+def workload_name(cfg):
+    if cfg.kind == "fv":
+        return f"{cfg.name}: 3D Euler patch FV {cfg.cells}^3 cells in {cfg.patch}^3 patches, CFL {cfg.cfl}"
+    what = "advection" if cfg.pde == "advection" else "Euler"
+    mesh = f"{cfg.cells}^{cfg.dim}" + (" + refined disc (2-level 3:1)" if cfg.kind == "dg-amr" else "")
+    return f"{cfg.name}: {cfg.dim}D {what} ADER-DG p={cfg.order} on {mesh}, CFL {cfg.cfl}/(2p+1)"
+
+
+def build_solver(cfg):
+    from paper_1806_07984_b200 import mesh as M, pde as P, solver as S
+    if cfg.kind == "fv":
+        s = S.FVSolver(P.euler(3), cfg.cells, cfg.patch, cfg.cfl, check_finite=False)
+        return s, cf.initial_fv(cfg), cfg.cells ** 3
+    pde = P.advection(cfg.velocity) if cfg.pde == "advection" else P.euler(cfg.dim)
+    if cfg.kind == "dg-amr":
+        mesh = M.AdaptiveMesh(cf.amr_cells(cfg), cfg.dim, cfg.periodic)
+        Q0 = cf.initial_dg_amr(cfg, mesh.cells)
+    else:
+        mesh = M.CartesianMesh(cfg.cells, cfg.dim, cfg.periodic)
+        Q0 = cf.initial_dg_uniform(cfg)
+    return S.DGSolver(pde, cfg.order, mesh, cfg.cfl, check_finite=False), Q0, mesh.ncells
+
+
+# ---------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ FP64 peak --
+
+def fp64_peak_tflops():
+    """Measured DFMA throughput (MEASURED_PEAKS.json carries no FP64 figure)."""
+    import ctypes
+    import torch
+    from paper_1806_07984_b200 import _lib
+    lib = _lib.load()
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = nsm * 8, 4096
+    best = 0.0
+    for _ in range(4):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.check(lib.edg_probe_fp64(_lib.ptr(sink), blocks, iters, st), "probe")
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        best = max(best, blocks * 256 * 8 * iters * 2 / (ms * 1e-3) / 1e12)
+    return best
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+# ----------------------------------------------------------- CPU (port) --
+
+_CPU = {}
+
+
+def _cpu_init(cfg_name, cfl):
+    cfg = cf.CONFIGS[cfg_name]
+    if cfl is not None:
+        cfg = cfg.with_(cfl=cfl)
+    from oracle import ops
+    _CPU["cfg"] = cfg
+    _CPU["Q"] = cf.initial_dg_uniform(cfg)
+    _CPU["pde"] = ops.euler(cfg.dim) if cfg.pde == "euler" else ops.advection(cfg.velocity)
+    _CPU["basis"] = ops.basis_for(cfg.order)
+
+
+def _cpu_chunk(args):
+    """Per-cell reference structure on a contiguous chunk of cells:
+    admissible-dt loop, stp_picard per cell, Rusanov per cell side, corrector
+    (kernels.py:120-281 restated in oracle/ops.py)."""
+    lo, hi, dt = args
+    from oracle import ops
+    cfg, Q, pde, b = _CPU["cfg"], _CPU["Q"], _CPU["pde"], _CPU["basis"]
+    N, d = cfg.cells, cfg.dim
+    h = 1.0 / N
+    edges = (h,) * d
+    t0 = time.perf_counter()
+    ops.stable_dt(((h, Q[c]) for c in range(lo, hi)), pde, cfg.order, cfg.cfl, d)
+    stores = {c: ops.predictor_picard(Q[c], pde, dt, b, edges) for c in range(lo, hi)}
+    strides = [N ** (d - 1 - t) for t in range(d)]
+    for c in range(lo, hi):
+        idx = [(c // strides[t]) % N for t in range(d)]
+        res = {}
+        for a in range(d):
+            for s in (0, 1):
+                j = idx[a] + (1 if s else -1)
+                nb = c + ((j % N) - idx[a]) * strides[a]
+                other = stores.get(nb, stores[c])
+                mine, theirs = stores[c].trace_q[(a, s)], other.trace_q[(a, 1 - s)]
+                lo_, hi_ = (mine, theirs) if s == 1 else (theirs, mine)
+                res[(a, s)] = ops.rusanov(lo_, hi_, pde, a)
+        ops.correct(stores[c], res, b, edges)
+    return hi - lo, time.perf_counter() - t0
+
+
+def cpu_port_rate(cfg_name, cfl, seconds, cores=None, steps=1):
+    """DoF-updates/s of the per-cell CPU port on a bounded cell sample; the
+    sample is sized for ~`seconds` of wall time per step on `cores` workers."""
+    import multiprocessing as mp
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    cfg = cf.CONFIGS[cfg_name] if cfl is None else cf.CONFIGS[cfg_name].with_(cfl=cfl)
+    _cpu_init(cfg_name, cfl)
+    from oracle import batched
+    Q = _CPU["Q"]
+    dt = batched.stable_dt_b(Q, 1.0 / cfg.cells, _CPU["pde"], cfg.order, cfg.cfl, cfg.dim)
+    cores = cores or os.cpu_count() or 1
+    probe = 16
+    n_probe, t_probe = _cpu_chunk((0, probe, dt))
+    per_cell = t_probe / n_probe
+    total = int(max(cores * 4, min(Q.shape[0], seconds * cores / per_cell)))
+    chunk = max(1, total // (cores * 4))
+    ctx = mp.get_context("fork")
+    rates = []
+    dof_cell = cfg.m * cfg.n ** cfg.dim
+    with ctx.Pool(cores, initializer=_cpu_init, initargs=(cfg_name, cfl)) as pool:
+        for k in range(steps):
+            start = (k * total) % max(1, Q.shape[0] - total)
+            jobs = [(start + i, min(start + i + chunk, start + total), dt) for i in range(0, total, chunk)]
+            t0 = time.perf_counter()
+            done = sum(n for n, _ in pool.map(_cpu_chunk, jobs))
+            rates.append(done * dof_cell / (time.perf_counter() - t0))
+    sample = (f"{total} of {Q.shape[0]} cells of step 1 per timed step (per-cell predictor + Rusanov + corrector "
+              f"+ dt loop), {cores} worker processes, OPENBLAS_NUM_THREADS=1")
+    return rates, cores, sample
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------- reference --
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    per_step = max(1.0, min(5.0, 150.0 / max(1, args.steps + args.warmup)))
+    if cfg.kind != "dg":
+        print(json.dumps({"impl": "reference", "unavailable": "CPU port sampler covers uniform DG configs only"}))
+        return
+    rates, cores, sample = cpu_port_rate(cfg.name, args.cfl, per_step, steps=args.warmup + args.steps)
+    timed = rates[args.warmup:]
+    value = statistics.median(timed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * cf.dof_count(cfg) / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs.py)",
+        "config": {"workload": workload_name(cfg), "cells": cfg.cells ** cfg.dim, "dof": cf.dof_count(cfg)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours --
+
+def run_ours(args, cfg):
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = dist_init(ws, "nccl")
+    from paper_1806_07984_b200 import solver as S
+
+    peak64 = fp64_peak_tflops()
+    solver, Q0, ncells = build_solver(cfg)
+    dof = cf.dof_count(cfg, ncells)
+    solver.set_state(Q0)
+    for _ in range(args.warmup):
+        solver.step()
+    torch.cuda.synchronize()
+    its0 = int(solver.iter_total.item()) if hasattr(solver, "iter_total") else 0
+    timer = S.KernelTimer()
+    solver.kernel_timer = timer
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record()
+        for _ in range(args.steps):
+            solver.step()
+        stop.record()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    solver.kernel_timer = None
+    ms = start.elapsed_time(stop)
+    ms_max = max_over_ranks(dist, ms, dev)
+    value = dof * args.steps * ws / (ms_max * 1e-3)
+    tot = timer.totals_ms()
+    status = solver.status.cpu().numpy()
+    hbm = measured_peaks().get("hbm_gbs")
+
+    kernels = {}
+    launches = 0
+    if cfg.kind == "fv":
+        n_fv, ms_fv = tot["fv"]
+        launches = args.steps * 2
+        cells = cfg.cells ** 3
+        byt = costs.fv_cell_bytes(cfg.m) * cells
+        ach = byt / (ms_fv / n_fv * 1e-3) / 1e9
+        kernels["fv_patch"] = {"ms_per_launch": ms_fv / n_fv, "bound": "hbm", "achieved": ach, "unit": "GB/s",
+                               "peak": hbm, "frac": ach / hbm if hbm else None,
+                               "gflops": costs.fv_cell_flops("euler") * cells / (ms_fv / n_fv * 1e-3) / 1e9}
+        roof = dict(kernels["fv_patch"], kernel="fv_patch")
+        iters_mean = None
+    elif "stp" not in tot:      # adaptive schedule: kernels run on two streams, no per-kernel events
+        its = int(solver.iter_total.item()) - its0
+        iters_mean = its / (args.steps * ncells)
+        launches = args.steps * 7
+        roof = {"bound": "fp64", "achieved": None, "peak": peak64, "unit": "TFLOP/s", "frac": None,
+                "kernel": "stp_picard"}
+    else:
+        d, n, m = cfg.dim, cfg.n, cfg.m
+        its = int(solver.iter_total.item()) - its0
+        iters_mean = its / (args.steps * ncells)
+        n_stp, ms_stp = tot["stp"]
+        flops = its * costs.stp_iter_flops(cfg.pde, d, n, m) + args.steps * ncells * costs.stp_epilogue_flops(
+            cfg.pde, d, n, m)
+        ach = flops / (ms_stp * 1e-3) / 1e12
+        kernels["stp_picard"] = {"ms_per_launch": ms_stp / n_stp, "bound": "fp64", "achieved": ach,
+                                 "unit": "TFLOP/s", "peak": peak64, "frac": ach / peak64,
+                                 "hbm_gbs": costs.stp_bytes(d, n, m) * ncells / (ms_stp / n_stp * 1e-3) / 1e9}
+        n_c, ms_c = tot["corrector"]
+        cb = costs.corrector_bytes(d, n, m) * ncells / (ms_c / n_c * 1e-3) / 1e9
+        kernels["corrector_fused"] = {"ms_per_launch": ms_c / n_c, "bound": "hbm", "achieved": cb, "unit": "GB/s",
+                                      "peak": hbm, "frac": cb / hbm if hbm else None}
+        launches = args.steps * 3
+        roof = dict(kernels["stp_picard"], kernel="stp_picard")
+    share = {k: v["ms_per_launch"] * args.steps / ms for k, v in kernels.items()}
+
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
+        traffic = tr.get(cfg.name, {}).get(roof["kernel"])
+    except (OSError, ValueError):
+        pass
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(solver, Q0, dof, args.steps, ws, dist, dev)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and cfg.kind == "dg":
+        rates, cores, sample = cpu_port_rate(cfg.name, args.cfl, args.cpu_seconds, steps=1)
+        cpu = {"value": rates[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+               "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs.py)",
+            "config": {"workload": workload_name(cfg), "cells": ncells, "dof": dof, "cfl_safety": cfg.cfl,
+                       "parallelism": f"replicas x{ws} (the path does not shard in this tier)",
+                       "steps_from_ic": f"{args.warmup + 1}..{args.warmup + args.steps}",
+                       "l2": "working set > 126 MB L2 (state + predictor buffers), no flush",
+                       "picard_iterations_mean": iters_mean,
+                       "nonfinite_cell_steps": int(status[1])},
+            "roofline": {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
+                         "unit": roof["unit"], "frac": roof["frac"], "traffic": traffic,
+                         "kernel": roof["kernel"],
+                         "peak_source": ("fp64: DFMA probe measured in this run (MEASURED_PEAKS.json has no FP64)"
+                                         if roof["bound"] == "fp64" else "MEASURED_PEAKS.json hbm_gbs")},
+            "kernels": kernels, "kernel_share_of_step": share,
+            "fp64_peak_tflops_measured": peak64,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def measure_e2e(solver, Q0, dof, steps, ws, dist, dev):
+    """Public API with host buffers: every step uploads the state from pinned
+    host memory (set_state), advances one step, downloads the result."""
+    import torch
+    host = torch.from_numpy(np.ascontiguousarray(Q0)).pin_memory()
+    out = torch.empty_like(host).pin_memory()
+    nb = host.numel() * 8
+    solver.set_state(host)
+    solver.step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        solver.set_state(host)
+        solver.step()
+        out.copy_(solver.state().reshape(out.shape), non_blocking=True)
+        host, out = out, host
+    b.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(dist, a.elapsed_time(b), dev)
+    return {"value": dof * steps * ws / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nb,
+            "d2h_bytes_per_step": nb, "ms_per_step": ms / steps,
+            "api": "DGSolver.set_state(pinned host) + step() + copy to pinned host"}
+
+
+def main():
+    args = parse()
+    cfg = cf.CONFIGS[args.config]
+    if args.cfl is not None:
+        cfg = cfg.with_(cfl=args.cfl)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

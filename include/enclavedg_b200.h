@@ -1,0 +1,185 @@
+/*
+ * enclavedg_b200 -- C ABI of the B200 (sm_100a) ADER-DG cell/face hot path.
+ *
+ * Drop-in boundary for the operator API of the reference package
+ * `enclavedg` (/root/reference/pkg/src/enclavedg).  The reference is pure
+ * Python/numpy and has no FFI; each entry point below replaces one reference
+ * function (cited file:line) and is what a ctypes/cffi binding of that
+ * function binds.  All pointers named *_dev are CUDA
+ * device pointers; everything else is host memory.  No torch types cross the
+ * boundary.  Every call is asynchronous on `stream` and returns a status.
+ *
+ * Layouts (reference kernels.py:5-10, component axis first):
+ *   cell DoFs   q[c][k][i0][i1][(i2)]        (C, m, n^d), last axis fastest
+ *   face traces t[c][2a+s][k][f]             (C, 2d, m, n^(d-1)); face (a, s)
+ *               keeps the non-normal axes in order
+ *   FV patches  P[b][k][x][y][z]             (B, m, k, k, k)
+ *
+ * Operators: `basis_dev` is a packed fp64 table built on the host by numpy
+ * exactly as the reference builds them (basis.py:34-65, kernels.py:109-114,
+ * transfer.py:28-39) and uploaded verbatim, offsets EDG_BASIS_*(n).
+ */
+#ifndef ENCLAVEDG_B200_H
+#define ENCLAVEDG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: errors.py:4-33 + SPEC.md:581 exit codes ---------------- */
+#define EDG_OK 0
+#define EDG_ERR_CONFIG 2     /* ConfigError: unsupported order / dim / pde     */
+#define EDG_ERR_NUMERICAL 3  /* NumericalError: non-finite state detected      */
+#define EDG_ERR_PROTOCOL 4   /* NotReadyError / AssertionError (missing data)  */
+#define EDG_ERR_CUDA 5       /* CUDA launch / runtime failure                  */
+#define EDG_ERR_NO_SPEED 6   /* EnclaveDgError: no positive wave speed         */
+
+/* ---- PDE plugin (pde.py:10-24); flux / max_eigenvalue are compiled in ----- */
+#define EDG_PDE_ADVECTION 0  /* pde.py:27-37 */
+#define EDG_PDE_BURGERS 1    /* pde.py:40-49 */
+#define EDG_PDE_EULER 2      /* added system */
+
+typedef struct {
+  int32_t kind;        /* EDG_PDE_* */
+  int32_t dim;         /* 2 or 3 */
+  int32_t m;           /* components: 1 (advection, burgers) or dim + 2 */
+  int32_t reserved;
+  double gamma;        /* Euler ratio of specific heats */
+  double velocity[3];  /* advection velocity */
+} edg_pde;
+
+/* packed operator table of one order, n = p + 1 nodes (doubles) */
+#define EDG_BASIS_D(n) 0                              /* D[i][j] = l_j'(x_i)   */
+#define EDG_BASIS_W(n) ((n) * (n))                    /* GL weights on [0,1]   */
+#define EDG_BASIS_TL(n) ((n) * (n) + (n))             /* l_j(0)                */
+#define EDG_BASIS_TR(n) ((n) * (n) + 2 * (n))         /* l_j(1)                */
+#define EDG_BASIS_KINV(n) ((n) * (n) + 3 * (n))       /* K^-1 (kernels.py:109) */
+#define EDG_BASIS_KLIFT(n) (2 * (n) * (n) + 3 * (n))  /* K^-1 @ lift           */
+#define EDG_BASIS_INTERP(n) (2 * (n) * (n) + 4 * (n)) /* interp[3][n][n]       */
+#define EDG_BASIS_RESTR(n) (5 * (n) * (n) + 4 * (n))  /* restrict[3][n][n]     */
+#define EDG_BASIS_SIZE(n) (8 * (n) * (n) + 4 * (n))
+
+/* Which (pde, dim, order) instantiations this build carries. */
+int edg_supported(const edg_pde* pde, int32_t order);
+/* Library version string and the CUDA arch it was compiled for. */
+const char* edg_build_info(void);
+
+/* ---- space-time predictor: stp_picard (kernels.py:120-159) --------------
+ * Processes the cells cell_list[0..nwork) (or cells 0..nwork) of q.  edges:
+ * device [dim] (edges_per_cell = 0) or [ncells][dim] (edges_per_cell = 1).
+ * dt_dev: device scalar.  Outputs are written at the cell's own index:
+ * q_end, q_int (nullable) (C,m,n^d); trace_q, trace_f (C,2d,m,n^(d-1));
+ * iterations (int32), converged (uint8).  max_iter <= 0 selects 2(p+1).
+ * iter_total_dev (nullable): += sum of the processed cells' iteration counts
+ * (used for algorithmic-flop accounting without a host round trip). */
+int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev,
+                   const double* q_dev, const int32_t* cell_list_dev, int32_t nwork,
+                   const double* edges_dev, int32_t edges_per_cell, const double* dt_dev,
+                   double tol, int32_t max_iter,
+                   double* q_end_dev, double* q_int_dev, double* trace_q_dev,
+                   double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev,
+                   unsigned long long* iter_total_dev, void* stream);
+
+/* ---- project_to_faces (kernels.py:73-79): vol (C,m,n^d) -> (C,2d,m,n^(d-1)) */
+int edg_project_to_faces(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t ncells,
+                         const double* vol_dev, double* traces_dev, void* stream);
+
+/* ---- riemann_rusanov on face batches (kernels.py:162-173) ----------------
+ * lo, hi, out: (nfaces, m, npts); sign >= 0 -> along +axis, else negated. */
+int edg_riemann_rusanov(const edg_pde* pde, int32_t nfaces, int32_t npts,
+                        const double* lo_dev, const double* hi_dev, int32_t axis,
+                        int32_t sign, double* out_dev, void* stream);
+
+/* ---- corrector (kernels.py:176-193) ---------------------------------------
+ * Generic form: side_face[c][2a+s] indexes outcomes (F, m, n^(d-1));
+ * a negative index is a missing outcome (EDG_ERR_PROTOCOL, reported through
+ * status_dev bit 1).  Fused Cartesian form (side_face == NULL): nbr[c][2a+s]
+ * is the face neighbour (-1 = outflow ghost, own trace) and the Rusanov
+ * outcome is evaluated inline (Riemann is exactly antisymmetric,
+ * kernels.py:165-173, so each face's two evaluations agree bitwise).
+ * Optionally fuses the next step's admissible-dt candidates
+ * (kernels.py:267-281) into dt_slots_dev (EDG_DT_SLOTS uint64 bit patterns,
+ * see edg_dt_finalize) using hmin_dev (per cell, or [1] when
+ * edges_per_cell == 0), and counts cells with a non-finite result in
+ * status_dev[1]. */
+#define EDG_DT_SLOTS 256
+int edg_corrector(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t ncells,
+                  const double* q_end_dev, const double* trace_q_dev, const double* trace_f_dev,
+                  const int32_t* nbr_dev, const int32_t* side_face_dev, const double* outcomes_dev,
+                  const double* edges_dev, int32_t edges_per_cell,
+                  double* q_out_dev, unsigned long long* dt_slots_dev, const double* hmin_dev,
+                  uint32_t* status_dev, void* stream);
+
+/* ---- admissible_dt (kernels.py:267-281) -----------------------------------
+ * edg_cell_speed_reduce: per-cell lambda (max over axes of max over nodes,
+ * NaN axes dropped like Python max) -> candidate h_c / ((2p+1) lambda_c) for
+ * cells with lambda > 0, min-reduced into dt_slots_dev.  `order` = p (0 for
+ * FV).  For FV patches pass npts = k^3 and q as (B, m, npts).
+ * edg_dt_finalize: dt = cfl * min(slots); writes dt_dev (and, when
+ * dt_hist_dev is non-null, dt_hist_dev[step] -- or, for step < 0,
+ * dt_hist_dev[status_dev[2]++] bounded by -step), re-arms the slots; no
+ * positive speed -> dt = NaN and status_dev[0] |= 1 (EDG_ERR_NO_SPEED).
+ * status_dev layout: [0] flags, [1] non-finite cells, [2] step counter. */
+int edg_cell_speed_reduce(const edg_pde* pde, int32_t order, int32_t ncells, int32_t npts,
+                          const double* q_dev, const double* hmin_dev, int32_t h_per_cell,
+                          unsigned long long* dt_slots_dev, void* stream);
+int edg_dt_slots_reset(unsigned long long* dt_slots_dev, void* stream);
+int edg_dt_finalize(unsigned long long* dt_slots_dev, double cfl, double* dt_dev,
+                    double* dt_hist_dev, int32_t step, uint32_t* status_dev, void* stream);
+
+/* ---- hanging faces (transfer.py:59-96) -------------------------------------
+ * edg_faces_rusanov: leaf faces f with axis[f], side cells cell[f][2],
+ * side kinds kind[f][2] (0 cell, 1 virtual = coarse owner's trace
+ * interpolated with interp[child_pos], 2 boundary = copy of the other side),
+ * child_pos[f][2] transverse digits.  Writes outcomes[f] (m, n^(d-1)).
+ * edg_faces_restrict: parent p accumulates, in child order,
+ * restrict[child_pos]-contracted outcomes of its 3^(d-1) children
+ * (children[p][j] face indices) into outcomes[parent_face[p]]. */
+int edg_faces_rusanov(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t nfaces,
+                      const int32_t* axis_dev, const int32_t* cell_dev, const int8_t* kind_dev,
+                      const int8_t* child_pos_dev, const double* trace_q_dev, double* outcomes_dev,
+                      void* stream);
+int edg_faces_restrict(int32_t dim, int32_t m, int32_t order, const double* basis_dev,
+                       int32_t nparents, const int32_t* parent_face_dev, const int32_t* children_dev,
+                       const int8_t* child_pos_dev, double* outcomes_dev, void* stream);
+/* interpolate_face_trace / restrict_face_values on batches (m, n^(d-1)). */
+int edg_interpolate_face_trace(int32_t dim, int32_t m, int32_t order, const double* basis_dev,
+                               int32_t nfaces, const double* trace_dev, const int8_t* child_pos_dev,
+                               int32_t restrict_mode, double* out_dev, void* stream);
+
+/* ---- finite volume: fv_patch_update (kernels.py:225-253) -------------------
+ * edg_fv_patch_update: per-patch API, halos (B, 2d, m, k^(d-1)) given.
+ * edg_fv_patch_step: patches of a Cartesian patch grid; halos are read from
+ * face-neighbour patches nbr[b][2a+s] (-1 = outflow: own boundary layer,
+ * kernels.py:256-264).  Optionally fuses the next step's dt candidates.
+ * edges: patch extent per axis (device [dim]). */
+int edg_fv_patch_update(const edg_pde* pde, int32_t k, int32_t npatches, const double* patch_dev,
+                        const double* halos_dev, const double* dt_dev, const double* edges_dev,
+                        double* out_dev, void* stream);
+int edg_fv_patch_step(const edg_pde* pde, int32_t k, int32_t npatches, const double* patch_dev,
+                      const int32_t* nbr_dev, const double* dt_dev, const double* edges_dev,
+                      double* out_dev, unsigned long long* dt_slots_dev, double h_cell,
+                      uint32_t* status_dev, void* stream);
+/* patch_boundary_layers (kernels.py:256-264): out (B, 2d, m, k^(d-1)). */
+int edg_patch_boundary_layers(int32_t dim, int32_t m, int32_t k, int32_t npatches,
+                              const double* patch_dev, double* out_dev, void* stream);
+
+/* ---- measurement helper: fp64 FMA throughput probe ----------------------
+ * Launches `blocks` x 256 threads, each running 8 independent DFMA chains of
+ * `iters` steps (flops = blocks * 256 * 8 * iters * 2).  Time it with events
+ * on `stream`; used by bench.py for the FP64 roofline denominator, which
+ * MEASURED_PEAKS.json does not carry. */
+int edg_probe_fp64(double* sink_dev, int32_t blocks, int32_t iters, void* stream);
+
+/* ---- stream schedule helpers --------------------------------------------- */
+/* Priority range of the device (numerically lower = higher priority). */
+int edg_stream_priority_range(int32_t* least, int32_t* greatest);
+/* Last CUDA error string of this thread (static storage). */
+const char* edg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENCLAVEDG_B200_H */

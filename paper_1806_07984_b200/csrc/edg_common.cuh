@@ -1,0 +1,158 @@
+// Shared device code of the enclavedg_b200 kernels (sm_100a, fp64).
+//
+// The pointwise PDE functions below evaluate exactly the operation sequence of
+// the reference plugins (pde.py:27-49) and of the Euler plugin pinned in
+// DESIGN.md, with the round-to-nearest intrinsics (__dmul_rn, __dadd_rn, ...)
+// that nvcc never contracts into FMAs; the results are therefore bit-identical
+// to numpy's on the same inputs.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/enclavedg_b200.h"
+
+namespace edg {
+
+constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+struct PdeParams {
+  double gamma;
+  double gm1;       // gamma - 1.0, computed on the host exactly like the oracle
+  double vel[3];
+};
+
+// ------------------------------------------------------------ PDE plugins --
+template <int KIND, int DIM>
+struct Pde;
+
+// pde.py:27-37: F_a = a_axis * q, lambda = |a_axis|
+template <int DIM>
+struct Pde<EDG_PDE_ADVECTION, DIM> {
+  static constexpr int M = 1;
+  struct Parts {};
+  __device__ __forceinline__ static Parts parts(const double*, const PdeParams&) { return {}; }
+  __device__ __forceinline__ static void flux(const double* q, const Parts&, int a, const PdeParams& pp,
+                                              double* f) {
+    f[0] = __dmul_rn(pp.vel[a], q[0]);
+  }
+  __device__ __forceinline__ static double lam(const double*, const Parts&, int a, const PdeParams& pp) {
+    return fabs(pp.vel[a]);
+  }
+};
+
+// pde.py:40-49: F = 0.5 * q * q (every axis), lambda = |q|
+template <int DIM>
+struct Pde<EDG_PDE_BURGERS, DIM> {
+  static constexpr int M = 1;
+  struct Parts {};
+  __device__ __forceinline__ static Parts parts(const double*, const PdeParams&) { return {}; }
+  __device__ __forceinline__ static void flux(const double* q, const Parts&, int, const PdeParams&,
+                                              double* f) {
+    f[0] = __dmul_rn(__dmul_rn(0.5, q[0]), q[0]);
+  }
+  __device__ __forceinline__ static double lam(const double* q, const Parts&, int, const PdeParams&) {
+    return fabs(q[0]);
+  }
+};
+
+// Euler (oracle/ops.py euler):
+//   inv = 1/rho; ke = (sum_i m_i*m_i) ; ke = (0.5*ke)*inv; p = gm1*(E - ke)
+//   u = m_a*inv; F = (m_a, m_i*u (+p on i = a), (E + p)*u); lambda = |u| + sqrt((gamma*p)*inv)
+template <int DIM>
+struct Pde<EDG_PDE_EULER, DIM> {
+  static constexpr int M = DIM + 2;
+  struct Parts {
+    double inv, p;
+  };
+  __device__ __forceinline__ static Parts parts(const double* q, const PdeParams& pp) {
+    Parts r;
+    r.inv = __drcp_rn(q[0]);
+    double ke = __dmul_rn(q[1], q[1]);
+#pragma unroll
+    for (int i = 1; i < DIM; ++i) ke = __dadd_rn(ke, __dmul_rn(q[1 + i], q[1 + i]));
+    ke = __dmul_rn(__dmul_rn(0.5, ke), r.inv);
+    r.p = __dmul_rn(pp.gm1, __dsub_rn(q[1 + DIM], ke));
+    return r;
+  }
+  // m_a without dynamic register indexing (a may be a runtime value)
+  __device__ __forceinline__ static double mom(const double* q, int a) {
+    double v = q[1];
+#pragma unroll
+    for (int i = 1; i < DIM; ++i) v = (a == i) ? q[1 + i] : v;
+    return v;
+  }
+  __device__ __forceinline__ static void flux(const double* q, const Parts& pr, int a, const PdeParams&,
+                                              double* f) {
+    const double ma = mom(q, a);
+    const double u = __dmul_rn(ma, pr.inv);
+    f[0] = ma;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      const double t = __dmul_rn(q[1 + i], u);
+      f[1 + i] = (i == a) ? __dadd_rn(t, pr.p) : t;
+    }
+    f[1 + DIM] = __dmul_rn(__dadd_rn(q[1 + DIM], pr.p), u);
+  }
+  __device__ __forceinline__ static double lam(const double* q, const Parts& pr, int a, const PdeParams& pp) {
+    const double u = __dmul_rn(mom(q, a), pr.inv);
+    const double c = __dsqrt_rn(__dmul_rn(__dmul_rn(pp.gamma, pr.p), pr.inv));
+    return __dadd_rn(fabs(u), c);
+  }
+};
+
+// np.maximum semantics: NaN if either operand is NaN.
+__device__ __forceinline__ double nan_max(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a > b ? a : b;
+}
+
+// Rusanov outcome along +axis (kernels.py:162-173), bit-exact numpy order:
+//   lam = maximum(l(lo), l(hi)); central = 0.5*(F(lo)+F(hi)); jump = 0.5*lam*(hi-lo)
+template <int KIND, int DIM>
+__device__ __forceinline__ void rusanov(const double* lo, const double* hi, int a, int sign,
+                                        const PdeParams& pp, double* out) {
+  using P = Pde<KIND, DIM>;
+  constexpr int M = P::M;
+  const auto pl = P::parts(lo, pp);
+  const auto ph = P::parts(hi, pp);
+  const double lam = nan_max(P::lam(lo, pl, a, pp), P::lam(hi, ph, a, pp));
+  double fl[M], fh[M];
+  P::flux(lo, pl, a, pp, fl);
+  P::flux(hi, ph, a, pp, fh);
+  const double hl = __dmul_rn(0.5, lam);
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    const double central = __dmul_rn(0.5, __dadd_rn(fl[k], fh[k]));
+    const double jump = __dmul_rn(hl, __dsub_rn(hi[k], lo[k]));
+    out[k] = sign >= 0 ? __dsub_rn(central, jump) : __dadd_rn(-central, jump);
+  }
+}
+
+// Bit pattern ordering for non-negative doubles / NaN-propagating max.
+__device__ __forceinline__ unsigned long long maxkey(double x) {
+  // x >= 0 or NaN; NaN (any sign) maps above +inf.
+  return (x != x) ? 0xFFFFFFFFFFFFFFFFull : (unsigned long long)__double_as_longlong(x);
+}
+__device__ __forceinline__ double from_maxkey(unsigned long long k) {
+  return k == 0xFFFFFFFFFFFFFFFFull ? __longlong_as_double(0x7FF8000000000000ll) : __longlong_as_double((long long)k);
+}
+
+constexpr unsigned long long DT_EMPTY = 0xFFFFFFFFFFFFFFFFull;   // no candidate yet
+
+// Python-max over axes of the per-axis node maxima (kernels.py:271-273):
+// lam = max(lam, ax) takes ax only if ax > lam, so a NaN axis is dropped.
+__device__ __forceinline__ double python_max(double lam, double ax) { return (ax > lam) ? ax : lam; }
+
+// candidate h / ((2p+1) * lam) (kernels.py:276-277)
+__device__ __forceinline__ double dt_candidate(double h, int order, double lam) {
+  return __ddiv_rn(h, __dmul_rn((double)(2 * order + 1), lam));
+}
+
+inline int check_launch() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? EDG_OK : EDG_ERR_CUDA;
+}
+
+}  // namespace edg

@@ -1,0 +1,5 @@
+// Instantiation unit: advection, dim 2 (see edg_unit.cuh).
+#define EDG_UNIT_KIND EDG_PDE_ADVECTION
+#define EDG_UNIT_DIM 2
+#define EDG_UNIT_NAME advection2
+#include "edg_unit.cuh"

@@ -1,0 +1,5 @@
+// Instantiation unit: euler, dim 2 (see edg_unit.cuh).
+#define EDG_UNIT_KIND EDG_PDE_EULER
+#define EDG_UNIT_DIM 2
+#define EDG_UNIT_NAME euler2
+#include "edg_unit.cuh"

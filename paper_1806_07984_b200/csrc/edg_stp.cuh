@@ -1,0 +1,327 @@
+// Space-time predictor (Picard) kernel -- replaces kernels.py:120-159.
+//
+// Mapping: one thread per spatial node, CPB cells per
+// CTA.  A thread keeps the whole time column of its node in registers
+// (qhat[n_t][m] and the next iterate acc[n_t][m]), so the K^-1 time
+// contraction is thread-local; the per-axis derivative contractions read the
+// flux of one time node from shared memory (double-buffered, one barrier per
+// time node), where all lanes of a pencil hit the same word (broadcast).
+//
+// Per Picard iteration and cell, with B[r][s] = K^-1[r][s] * (-dt w_s) and
+// c = K^-1 lift (kernels.py:134-142):
+//     acc[r] = c_r q + sum_s B[r][s] sum_a (D/h_a) (x)_a F_a(qhat_s)
+// then delta = max |acc - qhat| over the cell (NaN-propagating, via 64-bit
+// atomicMax on bit patterns) decides the per-cell exit exactly like
+// kernels.py:143-147 (delta < tol).  Converged cells stop updating; the CTA
+// runs until its last cell stops.  The epilogue (kernels.py:148-157) forms
+// q_end, q_int and the time-integrated flux, stages them in shared memory and
+// projects them onto the 2d faces.
+#pragma once
+#include "edg_common.cuh"
+
+namespace edg {
+
+struct StpArgs {
+  const double* q;
+  const int32_t* cell_list;
+  int32_t nwork;
+  const double* basis;
+  const double* edges;
+  int32_t edges_per_cell;
+  const double* dt;
+  double tol;
+  int32_t max_iter;
+  PdeParams pp;
+  double* q_end;
+  double* q_int;
+  double* trace_q;
+  double* trace_f;
+  int32_t* iterations;
+  uint8_t* converged;
+  unsigned long long* iter_total;   // optional: += sum of per-cell iterations
+};
+
+constexpr int stp_best_cpb(int npc, int target) {
+  if (npc >= target) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int c = 1; c * npc <= target + target / 4; ++c) {
+    const int thr = ((c * npc + 31) / 32) * 32;
+    const double eff = double(c * npc) / double(thr);
+    if (eff >= best_eff - 1e-9) {
+      best = c;
+      best_eff = eff;
+    }
+  }
+  return best;
+}
+
+template <int DIM, int N>
+struct StpCfg {
+  static constexpr int NPC = ipow(N, DIM);
+  static constexpr int NF = ipow(N, DIM - 1);
+  static constexpr int TARGET = DIM == 2 ? 256 : 128;
+  static constexpr int CPB = stp_best_cpb(NPC, TARGET);
+  static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32;
+};
+
+template <int KIND, int DIM, int N>
+struct StpSmem {
+  using C = StpCfg<DIM, N>;
+  static constexpr int M = Pde<KIND, DIM>::M;
+  static constexpr int OPS = 2 * N * N + 4 * N;                 // D, B, w, tr, tl, c
+  static constexpr int FB = C::CPB * DIM * M * C::NPC;          // one flux buffer
+  static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * FB) + sizeof(unsigned long long) * 2 * C::CPB;
+};
+
+// stride of axis a inside a cell's node block (last axis fastest)
+template <int DIM, int N>
+__device__ __forceinline__ constexpr int axis_stride(int a) {
+  return ipow(N, DIM - 1 - a);
+}
+
+// node index of face point f of face normal to axis a at normal index j
+template <int DIM, int N>
+__device__ __forceinline__ int face_node(int f, int a, int j) {
+  const int st = ipow(N, DIM - 1 - a);      // stride of axis a
+  const int hi = f / st;                    // axes before a
+  const int lo = f - hi * st;               // axes after a
+  return hi * st * N + j * st + lo;
+}
+
+template <int KIND, int DIM, int N>
+__global__ void __launch_bounds__(StpCfg<DIM, N>::THREADS)
+stp_picard_kernel(const StpArgs A) {
+  using P = Pde<KIND, DIM>;
+  using Cf = StpCfg<DIM, N>;
+  using Sm = StpSmem<KIND, DIM, N>;
+  constexpr int M = P::M;
+  constexpr int NPC = Cf::NPC;
+  constexpr int NF = Cf::NF;
+  constexpr int CPB = Cf::CPB;
+  constexpr int THREADS = Cf::THREADS;
+
+  extern __shared__ __align__(16) double smem[];
+  double* sD = smem;                 // D[N][N]
+  double* sB = sD + N * N;           // B[r][s]
+  double* sW = sB + N * N;
+  double* sTL = sW + N;
+  double* sTR = sTL + N;
+  double* sC = sTR + N;              // K^-1 lift
+  double* sF = sC + N;               // flux buffers [2][CPB][DIM][M][NPC]
+  unsigned long long* sRed = reinterpret_cast<unsigned long long*>(sF + 2 * Sm::FB);   // [2][CPB]
+
+  const int tid = threadIdx.x;
+  const int slot = tid / NPC;
+  const int node = tid - slot * NPC;
+  const int item = blockIdx.x * CPB + slot;
+  const bool has_cell = (slot < CPB) && (item < A.nwork);
+  const int cell = has_cell ? (A.cell_list ? A.cell_list[item] : item) : 0;
+  const double dt = *A.dt;
+
+  for (int i = tid; i < N * N; i += THREADS) {
+    sD[i] = A.basis[EDG_BASIS_D(N) + i];
+    const int s = i % N;
+    // B[r][s] = K^-1[r][s] * ((-dt) * w[s])   (kernels.py:141-142 folded)
+    sB[i] = A.basis[EDG_BASIS_KINV(N) + i] * (-dt * A.basis[EDG_BASIS_W(N) + s]);
+  }
+  for (int i = tid; i < N; i += THREADS) {
+    sW[i] = A.basis[EDG_BASIS_W(N) + i];
+    sTL[i] = A.basis[EDG_BASIS_TL(N) + i];
+    sTR[i] = A.basis[EDG_BASIS_TR(N) + i];
+    sC[i] = A.basis[EDG_BASIS_KLIFT(N) + i];
+  }
+  for (int i = tid; i < 2 * CPB; i += THREADS) sRed[i] = 0ull;
+  __syncthreads();
+
+  int ix[DIM];
+  {
+    int t = node;
+#pragma unroll
+    for (int a = DIM - 1; a >= 0; --a) {
+      ix[a] = t % N;
+      t /= N;
+    }
+  }
+  // derivative rows of this node, scaled by 1/h_a
+  double Dr[DIM][N];
+  {
+    const double* e = A.edges + (A.edges_per_cell ? (size_t)cell * DIM : 0);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const double ih = 1.0 / e[a];
+#pragma unroll
+      for (int j = 0; j < N; ++j) Dr[a][j] = sD[ix[a] * N + j] * ih;
+    }
+  }
+
+  double q0[M], qh[N][M], acc[N][M];
+  const size_t cbase = (size_t)cell * M * NPC;
+#pragma unroll
+  for (int k = 0; k < M; ++k) q0[k] = has_cell ? A.q[cbase + (size_t)k * NPC + node] : 1.0;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int k = 0; k < M; ++k) qh[r][k] = q0[k];
+
+  bool active = has_cell;
+  int its = 0;
+  bool conv = false;
+  const int max_iter = A.max_iter;
+
+  for (int it = 1; it <= max_iter; ++it) {
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int k = 0; k < M; ++k) acc[r][k] = sC[r] * q0[k];
+    }
+#pragma unroll
+    for (int s = 0; s < N; ++s) {
+      double* Fb = sF + (s & 1) * Sm::FB + slot * (DIM * M * NPC);
+      if (active) {
+        const auto pr = P::parts(qh[s], A.pp);
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          double f[M];
+          P::flux(qh[s], pr, a, A.pp, f);
+#pragma unroll
+          for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPC + node] = f[k];
+        }
+      }
+      __syncthreads();
+      if (active) {
+        double bcol[N];
+#pragma unroll
+        for (int r = 0; r < N; ++r) bcol[r] = sB[r * N + s];
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          double dv = 0.0;
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int st = ipow(N, DIM - 1 - a);
+            const double* Fa = Fb + (a * M + k) * NPC + (node - ix[a] * st);
+#pragma unroll
+            for (int j = 0; j < N; ++j) dv = fma(Dr[a][j], Fa[j * st], dv);
+          }
+#pragma unroll
+          for (int r = 0; r < N; ++r) acc[r][k] = fma(bcol[r], dv, acc[r][k]);
+        }
+      }
+    }
+    unsigned long long* red = sRed + (it & 1) * CPB;
+    if (active) {
+      unsigned long long mk = 0ull;
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const unsigned long long key = maxkey(fabs(acc[r][k] - qh[r][k]));
+          mk = key > mk ? key : mk;
+          qh[r][k] = acc[r][k];
+        }
+      atomicMax(red + slot, mk);
+    }
+    __syncthreads();
+    if (active) {
+      its = it;
+      const double delta = from_maxkey(red[slot]);
+      if (delta < A.tol) {
+        active = false;
+        conv = true;
+      }
+    }
+    if (tid < CPB) sRed[((it + 1) & 1) * CPB + tid] = 0ull;
+    if (!__syncthreads_or(active)) break;
+  }
+
+  // ---------------------------------------------------------- epilogue --
+  // q_end = sum_r l_r(1) qhat_r; q_int = dt sum_r w_r qhat_r;
+  // fint_a = dt sum_r w_r F_a(qhat_r)          (kernels.py:148-155)
+  double qe[M], qi[M], fi[DIM][M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    qe[k] = 0.0;
+    qi[k] = 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int k = 0; k < M; ++k) fi[a][k] = 0.0;
+  if (has_cell) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      const double tr = sTR[r], w = sW[r];
+      const auto pr = P::parts(qh[r], A.pp);
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        qe[k] = fma(tr, qh[r][k], qe[k]);
+        qi[k] = fma(w, qh[r][k], qi[k]);
+      }
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        double f[M];
+        P::flux(qh[r], pr, a, A.pp, f);
+#pragma unroll
+        for (int k = 0; k < M; ++k) fi[a][k] = fma(w, f[k], fi[a][k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      qi[k] *= dt;
+      A.q_end[cbase + (size_t)k * NPC + node] = qe[k];
+      if (A.q_int) A.q_int[cbase + (size_t)k * NPC + node] = qi[k];
+    }
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int k = 0; k < M; ++k) fi[a][k] *= dt;
+    if (node == 0) {
+      A.iterations[cell] = its;
+      A.converged[cell] = conv ? 1 : 0;
+    }
+  }
+  if (A.iter_total) {
+    // per-CTA sum of iteration counts (algorithmic-flop accounting), one atomic per CTA
+    __shared__ unsigned int sIts;
+    if (tid == 0) sIts = 0u;
+    __syncthreads();
+    if (has_cell && node == 0) atomicAdd(&sIts, (unsigned)its);
+    __syncthreads();
+    if (tid == 0 && sIts) atomicAdd(A.iter_total, (unsigned long long)sIts);
+  }
+  // stage q_int and fint for the face projections: [slot][(1+DIM)*M][NPC]
+  __syncthreads();
+  double* St = sF + slot * ((1 + DIM) * M * NPC);
+  if (has_cell) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) St[k * NPC + node] = qi[k];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int k = 0; k < M; ++k) St[((1 + a) * M + k) * NPC + node] = fi[a][k];
+  }
+  __syncthreads();
+  if (has_cell) {
+    constexpr int PER_FAM = 2 * DIM * M * NF;
+    const size_t tbase = (size_t)cell * PER_FAM;
+    for (int o = node; o < 2 * PER_FAM; o += NPC) {
+      const int fam = o / PER_FAM;
+      const int r = o - fam * PER_FAM;        // index inside [2d][M][NF]
+      const int fs = r / (M * NF);
+      const int k = (r / NF) % M;
+      const int f = r % NF;
+      const int a = fs >> 1, s = fs & 1;
+      const double* src = St + ((fam == 0 ? 0 : (1 + a) * M) + k) * NPC;
+      const double* tv = s ? sTR : sTL;
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) v = fma(tv[j], src[face_node<DIM, N>(f, a, j)], v);
+      (fam == 0 ? A.trace_q : A.trace_f)[tbase + r] = v;
+    }
+  }
+}
+
+}  // namespace edg

@@ -1,0 +1,149 @@
+// One compilation unit per (PDE kind, dimension): instantiates every
+// PDE-specialised kernel for the supported node counts and exposes host-side
+// launchers edg::unit_<name>_*.  Included by edg_k_*.cu with EDG_UNIT_KIND,
+// EDG_UNIT_DIM and EDG_UNIT_NAME defined (split for parallel nvcc builds).
+#include "edg_stp.cuh"
+#include "edg_faces.cuh"
+#include "edg_fv.cuh"
+#include "edg_dt.cuh"
+
+#define EDG_CAT2(a, b) a##b
+#define EDG_CAT(a, b) EDG_CAT2(a, b)
+#define EDG_FN(suffix) EDG_CAT(EDG_CAT(unit_, EDG_UNIT_NAME), suffix)
+
+#if EDG_UNIT_DIM == 2
+#define EDG_FOR_N(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
+#else
+#define EDG_FOR_N(X) X(2) X(3) X(4) X(5) X(6)
+#endif
+
+namespace edg {
+
+template <typename K>
+static int set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+      return EDG_ERR_CUDA;
+  }
+  return EDG_OK;
+}
+
+template <int N>
+static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
+  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  using Cf = StpCfg<DIM, N>;
+  const size_t smem = StpSmem<KIND, DIM, N>::BYTES;
+  auto kern = stp_picard_kernel<KIND, DIM, N>;
+  if (set_smem(kern, smem)) return EDG_ERR_CUDA;
+  const int blocks = (a.nwork + Cf::CPB - 1) / Cf::CPB;
+  if (blocks > 0) kern<<<blocks, Cf::THREADS, smem, st>>>(a);
+  return check_launch();
+}
+
+int EDG_FN(_stp)(int n, const StpArgs& a, cudaStream_t st) {
+  switch (n) {
+#define EDG_CASE(NN) \
+  case NN:           \
+    return launch_stp_n<NN>(a, st);
+    EDG_FOR_N(EDG_CASE)
+#undef EDG_CASE
+  }
+  return EDG_ERR_CONFIG;
+}
+
+template <int N>
+static int launch_corr_n(bool fused, const CorrArgs& a, cudaStream_t st) {
+  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  using Cf = CorrCfg<DIM, N>;
+  const size_t smem = CorrSmem<KIND, DIM, N>::BYTES;
+  const int blocks = (a.ncells + Cf::CPB - 1) / Cf::CPB;
+  if (blocks <= 0) return EDG_OK;
+  if (fused) {
+    auto kern = corrector_kernel<KIND, DIM, N, true>;
+    if (set_smem(kern, smem)) return EDG_ERR_CUDA;
+    kern<<<blocks, Cf::THREADS, smem, st>>>(a);
+  } else {
+    auto kern = corrector_kernel<KIND, DIM, N, false>;
+    if (set_smem(kern, smem)) return EDG_ERR_CUDA;
+    kern<<<blocks, Cf::THREADS, smem, st>>>(a);
+  }
+  return check_launch();
+}
+
+int EDG_FN(_corr)(int n, bool fused, const CorrArgs& a, cudaStream_t st) {
+  switch (n) {
+#define EDG_CASE(NN) \
+  case NN:           \
+    return launch_corr_n<NN>(fused, a, st);
+    EDG_FOR_N(EDG_CASE)
+#undef EDG_CASE
+  }
+  return EDG_ERR_CONFIG;
+}
+
+int EDG_FN(_faces)(int n, const FaceArgs& a, cudaStream_t st) {
+  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  switch (n) {
+#define EDG_CASE(NN)                                                                      \
+  case NN: {                                                                              \
+    const long long work = (long long)a.nfaces * ipow(NN, DIM - 1);                       \
+    if (work > 0) faces_rusanov_kernel<KIND, DIM, NN><<<(unsigned)((work + 127) / 128), 128, 0, st>>>(a); \
+    return check_launch();                                                                \
+  }
+    EDG_FOR_N(EDG_CASE)
+#undef EDG_CASE
+  }
+  return EDG_ERR_CONFIG;
+}
+
+int EDG_FN(_speed)(int order, int ncells, int npts, const double* q, const double* hmin, int h_per_cell,
+                   unsigned long long* slots, const PdeParams& pp, cudaStream_t st) {
+  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  if (ncells > 0)
+    cell_speed_kernel<KIND, DIM><<<(ncells + 7) / 8, 256, 0, st>>>(ncells, npts, q, hmin, h_per_cell, order, slots, pp);
+  return check_launch();
+}
+
+int EDG_FN(_riemann)(int nfaces, int npts, const double* lo, const double* hi, int axis, int sign, double* out,
+                     const PdeParams& pp, cudaStream_t st) {
+  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  const long long work = (long long)nfaces * npts;
+  if (work > 0)
+    riemann_batch_kernel<KIND, DIM><<<(unsigned)((work + 255) / 256), 256, 0, st>>>(nfaces, npts, lo, hi, axis, sign,
+                                                                                  out, pp);
+  return check_launch();
+}
+
+template <int K>
+static int launch_fv_k(const FvArgs& a, cudaStream_t st) {
+  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  const size_t smem = FvSmem<KIND, DIM, K>::BYTES;
+  auto kern = fv_patch_kernel<KIND, DIM, K>;
+  if (set_smem(kern, smem)) return EDG_ERR_CUDA;
+  if (a.npatches > 0) kern<<<a.npatches, FvCfg<DIM, K>::THREADS, smem, st>>>(a);
+  return check_launch();
+}
+
+int EDG_FN(_fv)(int k, const FvArgs& a, cudaStream_t st) {
+  switch (k) {
+    case 3:
+      return launch_fv_k<3>(a, st);
+    case 5:
+      return launch_fv_k<5>(a, st);
+    case 7:
+      return launch_fv_k<7>(a, st);
+    case 8:
+      return launch_fv_k<8>(a, st);
+  }
+  return EDG_ERR_CONFIG;
+}
+
+int EDG_FN(_max_n)() {
+#if EDG_UNIT_DIM == 2
+  return 8;
+#else
+  return 6;
+#endif
+}
+
+}  // namespace edg

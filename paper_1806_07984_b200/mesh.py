@@ -1,0 +1,186 @@
+"""Host-side static mesh topology, exported once as index arrays for the GPU.
+
+Two mesh kinds cover the BASELINE configurations:
+
+* CartesianMesh -- uniform N^d cells, periodic or outflow, row-major cell
+  order (configs 1-4; the reference's 3-partitioned tree only offers 3^k,
+  SURVEY.md section 0).  Exports nbr[c][2a+s] (-1 = outflow).
+* AdaptiveMesh -- a static mesh of real cells (level, index) with at most one
+  level between face neighbours (config 5), in the reference's SFC order.
+  Builds the same face forest as the reference Mesh (mesh.py:346-483): a
+  coarse face whose other side is refined becomes a parent with 3^(d-1)
+  child faces in child_pos order, each child face having the fine cell on
+  one side and a virtual side (the coarse owner's trace interpolated,
+  transfer.py:75-79) on the other.  Exports the leaf-face list, the parent
+  list and side_face[c][2a+s] (an index into the outcome array: leaves
+  first, then parents), plus the skeleton / enclave split of the schedule.
+
+Skeleton rule (BASELINE.json config 5, pinned in DESIGN.md): a cell is
+skeleton iff one of its faces is hanging (coarse side of a parent face -- the
+reference classify_cell, mesh.py:585-596 -- or fine side of a child face) or
+its closure meets the synthetic partition cut x = 0.5.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+from .errors import ConfigError
+
+
+def _row_major_strides(N, dim):
+    return [N ** (dim - 1 - t) for t in range(dim)]
+
+
+class CartesianMesh:
+    def __init__(self, N: int, dim: int, periodic: bool, extent: float = 1.0):
+        if dim not in (2, 3):
+            raise ConfigError(f"dim must be 2 or 3, got {dim}")
+        self.N, self.dim, self.periodic = N, dim, periodic
+        self.h = extent / N
+        self.ncells = N ** dim
+        idx = np.stack(np.meshgrid(*[np.arange(N)] * dim, indexing="ij"), axis=-1).reshape(-1, dim)
+        strides = np.array(_row_major_strides(N, dim))
+        nbr = np.empty((self.ncells, 2 * dim), dtype=np.int32)
+        for a in range(dim):
+            for s in (0, 1):
+                j = idx[:, a] + (1 if s else -1)
+                ok = (j >= 0) & (j < N)
+                jw = j % N
+                nb = (idx.copy())
+                nb[:, a] = jw
+                lin = (nb * strides).sum(axis=1)
+                if not periodic:
+                    lin = np.where(ok, lin, -1)
+                nbr[:, 2 * a + s] = lin
+        self.index = idx
+        self.nbr = nbr
+
+    def cell_edges(self, level=None):
+        return (self.h,) * self.dim
+
+
+class AdaptiveMesh:
+    def __init__(self, cells, dim: int, periodic: bool, extent: float = 1.0, cut_x=0.5):
+        if dim not in (2, 3):
+            raise ConfigError(f"dim must be 2 or 3, got {dim}")
+        self.dim, self.periodic, self.extent = dim, periodic, extent
+        cells = [(int(l), tuple(int(i) for i in ix)) for l, ix in cells]
+        self.cells = sorted(cells, key=self._sfc_key)
+        self.ncells = len(self.cells)
+        self.pos = {c: i for i, c in enumerate(self.cells)}
+        self.levels = np.array([l for l, _ in self.cells], dtype=np.int32)
+        h = extent / 3.0 ** self.levels
+        self.edges = np.repeat(h[:, None], dim, axis=1)
+        self.hmin = h.copy()
+        self.cut_x = cut_x
+        self._build()
+
+    def cell_edges(self, level):
+        return tuple(self.extent / 3 ** level for _ in range(self.dim))
+
+    def _sfc_key(self, cell):
+        level, idx = cell
+        return tuple(tuple((idx[t] // 3 ** (level - l)) % 3 for t in range(self.dim)) for l in range(1, level + 1))
+
+    def _covering(self, level, idx):
+        """Real cell at level <= `level` covering idx, or None if refined."""
+        for lev in range(level, -1, -1):
+            key = (lev, tuple(i // 3 ** (level - lev) for i in idx))
+            if key in self.pos:
+                return key
+        return None
+
+    def _build(self):
+        d = self.dim
+        leaf = {}          # key -> dict(axis, cells[2], kinds[2], child_pos)
+        parents = {}       # key -> list of child keys
+        side_key = {}      # (cell, fs) -> face key (leaf or parent)
+        for c in self.cells:
+            level, idx = c
+            n = 3 ** level
+            for a in range(d):
+                for s in (0, 1):
+                    j = idx[a] + (1 if s else -1)
+                    if not (0 <= j < n) and not self.periodic:
+                        key = ("L", a, level, idx[:a] + (idx[a] + s,) + idx[a + 1:])
+                        leaf[key] = dict(axis=a, cells=[self.pos[c], self.pos[c]],
+                                         kinds=[2, 0] if s == 0 else [0, 2], child_pos=(0, 0))
+                        side_key[(c, 2 * a + s)] = key
+                        continue
+                    nb = idx[:a] + (j % n,) + idx[a + 1:]
+                    cov = self._covering(level, nb)
+                    up = idx[a] + s
+                    if self.periodic and up == n:
+                        up = 0
+                    fpos = idx[:a] + (up,) + idx[a + 1:]
+                    if cov is not None and cov[0] == level:
+                        key = ("L", a, level, fpos)
+                        lo, hi = (c, cov) if s == 1 else (cov, c)
+                        leaf[key] = dict(axis=a, cells=[self.pos[lo], self.pos[hi]], kinds=[0, 0], child_pos=(0, 0))
+                        side_key[(c, 2 * a + s)] = key
+                    elif cov is not None:
+                        if cov[0] != level - 1:
+                            raise ConfigError("AdaptiveMesh supports one level between face neighbours")
+                        # this fine cell sits on a child face of the coarse neighbour's face
+                        digits = tuple(idx[t] % 3 for t in range(d) if t != a)
+                        key = ("L", a, level, fpos)
+                        lo, hi = (c, cov) if s == 1 else (cov, c)
+                        kinds = [0, 1] if s == 1 else [1, 0]
+                        leaf[key] = dict(axis=a, cells=[self.pos[lo], self.pos[hi]], kinds=kinds,
+                                         child_pos=digits + (0,) * (2 - len(digits)))
+                        side_key[(c, 2 * a + s)] = key
+                        # parent face key of the coarse cell side (a, 1 - s)
+                        cl, ci = cov
+                        cn = 3 ** cl
+                        cup = ci[a] + (1 - s)
+                        if self.periodic and cup == cn:
+                            cup = 0
+                        pkey = ("P", a, cl, ci[:a] + (cup,) + ci[a + 1:])
+                        parents.setdefault(pkey, {})[digits] = key
+                    else:
+                        key = ("P", a, level, fpos)
+                        parents.setdefault(key, {})
+                        side_key[(c, 2 * a + s)] = key
+        # coarse cells' sides on parents
+        nch = 3 ** (d - 1)
+        for pkey, ch in parents.items():
+            if len(ch) != nch:
+                raise ConfigError(f"parent face {pkey} has {len(ch)} children, expected {nch}")
+        # classification (needs the face kinds), then the face order:
+        # skeleton-only leaves first so each schedule phase is a contiguous range
+        self.hanging = np.zeros(self.ncells, dtype=bool)
+        for rec in leaf.values():
+            if 1 in rec["kinds"]:
+                self.hanging[rec["cells"]] = True
+        x0 = np.array([ix[0] for _, ix in self.cells]) * self.hmin
+        x1 = x0 + self.hmin
+        cut = np.zeros(self.ncells, dtype=bool) if self.cut_x is None else (x0 <= self.cut_x) & (self.cut_x <= x1)
+        self.skeleton_mask = self.hanging | cut
+        self.skeleton = np.nonzero(self.skeleton_mask)[0].astype(np.int32)
+        self.enclave = np.nonzero(~self.skeleton_mask)[0].astype(np.int32)
+        on_skel = {k: bool(self.skeleton_mask[rec["cells"]].all()) for k, rec in leaf.items()}
+        leaf_keys = sorted(leaf, key=lambda k: (not on_skel[k], k[1], k[2], k[3]))
+        self.nleaf_skeleton = sum(on_skel.values())
+        par_keys = sorted(parents, key=lambda k: (k[1], k[2], k[3]))
+        index = {k: i for i, k in enumerate(leaf_keys)}
+        F = len(leaf_keys)
+        for i, k in enumerate(par_keys):
+            index[k] = F + i
+        self.nleaf, self.nparent = F, len(par_keys)
+        self.face_axis = np.array([leaf[k]["axis"] for k in leaf_keys], dtype=np.int32)
+        self.face_cell = np.array([leaf[k]["cells"] for k in leaf_keys], dtype=np.int32).reshape(F, 2)
+        self.face_kind = np.array([leaf[k]["kinds"] for k in leaf_keys], dtype=np.int8).reshape(F, 2)
+        self.face_child_pos = np.array([leaf[k]["child_pos"] for k in leaf_keys], dtype=np.int8).reshape(F, 2)
+        digits_all = list(itertools.product(range(3), repeat=d - 1))
+        self.parent_face = np.arange(F, F + self.nparent, dtype=np.int32)
+        self.parent_children = np.array([[index[parents[k][dg]] for dg in digits_all] for k in par_keys],
+                                        dtype=np.int32).reshape(self.nparent, nch)
+        if self.nparent and self.parent_children.max() >= self.nleaf_skeleton:
+            raise ConfigError("internal: a hanging child face is not on the skeleton")
+        self.side_face = np.full((self.ncells, 2 * d), -1, dtype=np.int32)
+        for (c, fs), k in side_key.items():
+            self.side_face[self.pos[c], fs] = index[k]
+        if (self.side_face < 0).any():
+            raise ConfigError("internal: cell side without a face")

@@ -1,0 +1,343 @@
+"""Time-step drivers on the GPU: the single-GPU replacement of the
+reference's Algorithm-1 loop and of the enclave task
+runtime.
+
+DGSolver (uniform Cartesian or static adaptive mesh) and FVSolver keep all
+state resident in HBM.  One step is a fixed sequence of kernel launches with
+no host synchronisation -- dt is reduced and consumed on the device
+(edg_dt_finalize) -- so a run of steps can be captured once into a CUDA
+graph and replayed.
+
+Uniform step (configs 1-3):   dt_finalize -> STP(all cells) -> fused
+                              Riemann+corrector(+next-dt candidates)
+Adaptive step (config 5), skeleton-first two-priority-stream schedule:
+    main:    dt_finalize -> fork
+    high:    STP(skeleton) -> faces/restrict of skeleton-only faces (incl. all hanging faces)
+    low:     STP(enclave)
+    main:    join -> faces of the remaining faces -> corrector(+dt)
+FV step (config 4):           dt_finalize -> patch update(+next-dt candidates)
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .basis import get_basis
+from .errors import ConfigError, EnclaveDgError, NumericalError
+from .kernels import _check_supported, _stream, _torch
+from .mesh import AdaptiveMesh, CartesianMesh
+from .pde import PdeDescriptor
+
+
+class KernelTimer:
+    """CUDA-event pairs around named kernel launches on the launching stream."""
+
+    def __init__(self):
+        self.pairs = {}
+        self._open = {}
+
+    def begin(self, name):
+        torch = _torch()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream())
+        self._open[name] = e
+
+    def end(self, name):
+        torch = _torch()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream())
+        self.pairs.setdefault(name, []).append((self._open.pop(name), e))
+
+    def totals_ms(self):
+        """{name: (launches, total ms)} -- call after a synchronize."""
+        return {k: (len(v), sum(a.elapsed_time(b) for a, b in v)) for k, v in self.pairs.items()}
+
+
+class _Base:
+    def _common_alloc(self, max_steps):
+        torch = self.torch
+        self.dt = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self.dt_hist = torch.zeros(max_steps, dtype=torch.float64, device="cuda")
+        self.slots = torch.empty(_lib.DT_SLOTS, dtype=torch.int64, device="cuda")
+        self.status = torch.zeros(4, dtype=torch.int32, device="cuda")
+        self.steps_done = 0
+        self.max_steps = max_steps
+        self._graph = None
+        self._graph_steps = 0
+        self.kernel_timer = None      # optional KernelTimer (events around the hot kernels)
+
+    def _finalize_dt(self):
+        """dt = cfl * min(candidates of the current state) (kernels.py:281);
+        the device step counter status[2] indexes the dt history."""
+        _lib.check(self.lib.edg_dt_finalize(_lib.ptr(self.slots), float(self.cfl), _lib.ptr(self.dt),
+                                            _lib.ptr(self.dt_hist), -self.max_steps, _lib.ptr(self.status),
+                                            _stream()), "dt_finalize")
+
+    def check_status(self):
+        st = self.status.cpu().numpy()
+        if st[0] & 1:
+            raise EnclaveDgError("no positive wave speed anywhere; cannot pick a time step")
+        if st[0] & 2:
+            raise AssertionError("face outcome missing (ordering bug)")
+        if self.check_finite and st[1] > 0:
+            raise NumericalError(f"{int(st[1])} cell(s) with a non-finite state")
+        return st
+
+    def dt_history(self):
+        return self.dt_hist[:min(self.steps_done, self.max_steps)].cpu().numpy()
+
+    # ------------------------------------------------------------- graphs --
+    def run(self, steps: int, graph: bool = True, chunk: int = 2):
+        """Advance `steps` steps.  With graph=True the launches of `chunk`
+        consecutive steps are captured once into a CUDA graph and replayed
+        (chunk must be even so the double buffers return to their roles)."""
+        torch = self.torch
+        if not graph:
+            for _ in range(steps):
+                self.step()
+            return
+        if chunk % 2:
+            raise ConfigError("graph chunk must be even (ping-pong buffers)")
+        full = steps // chunk
+        if full and self.steps_done + full * chunk > self.max_steps:
+            raise ConfigError("dt history too short: raise max_steps")
+        if full:
+            if self._graph is None or self._graph_steps != chunk:
+                # capture from a step whose parity matches replay
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                g = torch.cuda.CUDAGraph()
+                base = self.steps_done
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(g, stream=side):
+                        for k in range(chunk):
+                            self._enqueue_step()
+                torch.cuda.current_stream().wait_stream(side)
+                self._graph, self._graph_steps = g, chunk
+                self.steps_done = base          # capture does not execute
+            for _ in range(full):
+                self._graph.replay()
+                self.steps_done += chunk
+        for _ in range(steps - full * chunk):
+            self.step()
+
+    def step(self):
+        self._enqueue_step()
+        self.steps_done += 1
+
+
+class DGSolver(_Base):
+    """ADER-DG time stepping on the GPU (Algorithm 1 semantics)."""
+
+    def __init__(self, pde: PdeDescriptor, order: int, mesh, cfl: float, tol: float = 1e-10, max_iter=None,
+                 check_finite: bool = True, max_steps: int = 4096, two_streams: bool = True):
+        torch = self.torch = _torch()
+        self.lib = _lib.load()
+        _check_supported(pde, order)
+        self.pde, self.order, self.mesh, self.cfl = pde, order, mesh, float(cfl)
+        self.tol = float(tol)
+        self.max_iter = 0 if max_iter is None else int(max_iter)
+        self.check_finite = check_finite
+        self.basis = get_basis(order)
+        self.table = self.basis.device_table()
+        self.native = pde.native()
+        d, m, n = pde.dim, pde.m, self.basis.n
+        if mesh.dim != d:
+            raise ConfigError("mesh and pde dimension differ")
+        Cn = self.ncells = mesh.ncells
+        f64 = dict(dtype=torch.float64, device="cuda")
+        self.Q = torch.zeros((Cn, m) + (n,) * d, **f64)
+        self.Qn = torch.zeros_like(self.Q)
+        self.q_end = torch.zeros_like(self.Q)
+        self.trace_q = torch.zeros((Cn, 2 * d, m) + (n,) * (d - 1), **f64)
+        self.trace_f = torch.zeros_like(self.trace_q)
+        self.iterations = torch.zeros(Cn, dtype=torch.int32, device="cuda")
+        self.converged = torch.zeros(Cn, dtype=torch.uint8, device="cuda")
+        self.iter_total = torch.zeros(1, dtype=torch.int64, device="cuda")   # sum of Picard iterations
+        self._common_alloc(max_steps)
+        self.adaptive = isinstance(mesh, AdaptiveMesh)
+        i32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()  # noqa: E731
+        if self.adaptive:
+            self.edges = torch.from_numpy(mesh.edges.copy()).cuda()
+            self.edges_per_cell = 1
+            self.hmin = torch.from_numpy(mesh.hmin.copy()).cuda()
+            self.face_axis = i32(mesh.face_axis)
+            self.face_cell = i32(mesh.face_cell)
+            self.face_kind = torch.from_numpy(mesh.face_kind.copy()).cuda()
+            self.face_cp = torch.from_numpy(mesh.face_child_pos.copy()).cuda()
+            self.side_face = i32(mesh.side_face)
+            self.outcomes = torch.zeros((mesh.nleaf + mesh.nparent, m) + (n,) * (d - 1), **f64)
+            self.skel = i32(mesh.skeleton)
+            self.encl = i32(mesh.enclave)
+            self.parent_face = i32(mesh.parent_face)
+            self.parent_children = i32(mesh.parent_children)
+            self.nface_sk = mesh.nleaf_skeleton
+            self.two_streams = two_streams
+            if two_streams:
+                lo, hi = C.c_int32(), C.c_int32()
+                _lib.check(self.lib.edg_stream_priority_range(C.byref(lo), C.byref(hi)), "priority range")
+                try:
+                    self.s_hi = torch.cuda.Stream(priority=hi.value)
+                except (RuntimeError, ValueError):
+                    self.s_hi = torch.cuda.Stream(priority=-1)
+                self.s_lo = torch.cuda.Stream(priority=lo.value)
+        else:
+            self.edges = torch.tensor([mesh.h] * d, **f64)
+            self.edges_per_cell = 0
+            self.hmin = torch.tensor([mesh.h], **f64)
+            self.nbr = i32(mesh.nbr)
+
+    # ---------------------------------------------------------------- state --
+    def set_state(self, Q):
+        torch = self.torch
+        src = Q if isinstance(Q, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(Q, dtype=np.float64))
+        self.Q.copy_(src.reshape(self.Q.shape), non_blocking=True)
+        self.steps_done = 0
+        self.status.zero_()
+        self._seed_dt()
+
+    def _seed_dt(self):
+        """Candidates of the current state (the corrector refreshes them every step)."""
+        lib = self.lib
+        _lib.check(lib.edg_dt_slots_reset(_lib.ptr(self.slots), _stream()), "dt reset")
+        npts = self.basis.n ** self.pde.dim
+        _lib.check(lib.edg_cell_speed_reduce(C.byref(self.native), self.order, self.ncells, npts, _lib.ptr(self.Q),
+                                             _lib.ptr(self.hmin), self.edges_per_cell, _lib.ptr(self.slots),
+                                             _stream()), "admissible_dt")
+
+    def state(self):
+        return self.Q
+
+    # ----------------------------------------------------------------- step --
+    def _stp(self, cell_list, nwork):
+        return self.lib.edg_stp_picard(C.byref(self.native), self.order, _lib.ptr(self.table), _lib.ptr(self.Q),
+                                       _lib.ptr(cell_list), nwork, _lib.ptr(self.edges), self.edges_per_cell,
+                                       _lib.ptr(self.dt), self.tol, self.max_iter, _lib.ptr(self.q_end), None,
+                                       _lib.ptr(self.trace_q), _lib.ptr(self.trace_f), _lib.ptr(self.iterations),
+                                       _lib.ptr(self.converged), _lib.ptr(self.iter_total), _stream())
+
+    def _faces(self, off, cnt):
+        """Rusanov on leaf faces [off, off + cnt) (skeleton-only faces come first)."""
+        if cnt <= 0:
+            return
+        sl = slice(off, off + cnt)
+        _lib.check(self.lib.edg_faces_rusanov(C.byref(self.native), self.order, _lib.ptr(self.table), cnt,
+                                              _lib.ptr(self.face_axis[sl]), _lib.ptr(self.face_cell[sl]),
+                                              _lib.ptr(self.face_kind[sl]), _lib.ptr(self.face_cp[sl]),
+                                              _lib.ptr(self.trace_q), _lib.ptr(self.outcomes[sl]), _stream()),
+                   "faces_rusanov")
+
+    def _restrict(self):
+        _lib.check(self.lib.edg_faces_restrict(self.pde.dim, self.pde.m, self.order, _lib.ptr(self.table),
+                                               self.mesh.nparent, _lib.ptr(self.parent_face),
+                                               _lib.ptr(self.parent_children), _lib.ptr(self.face_cp),
+                                               _lib.ptr(self.outcomes), _stream()), "faces_restrict")
+
+    def _enqueue_step(self):
+        torch = self.torch
+        lib = self.lib
+        self._finalize_dt()
+        tm = self.kernel_timer
+        if not self.adaptive:
+            if tm:
+                tm.begin("stp")
+            _lib.check(self._stp(None, self.ncells), "stp_picard")
+            if tm:
+                tm.end("stp")
+                tm.begin("corrector")
+            _lib.check(lib.edg_corrector(C.byref(self.native), self.order, _lib.ptr(self.table), self.ncells,
+                                         _lib.ptr(self.q_end), _lib.ptr(self.trace_q), _lib.ptr(self.trace_f),
+                                         _lib.ptr(self.nbr), None, None, _lib.ptr(self.edges), self.edges_per_cell,
+                                         _lib.ptr(self.Qn), _lib.ptr(self.slots), _lib.ptr(self.hmin),
+                                         _lib.ptr(self.status), _stream()), "corrector")
+            if tm:
+                tm.end("corrector")
+        else:
+            nsk, F = self.nface_sk, self.mesh.nleaf
+
+            def skeleton_phase():
+                _lib.check(self._stp(self.skel, int(self.skel.numel())), "stp_picard(skeleton)")
+                self._faces(0, nsk)
+                self._restrict()
+
+            def enclave_phase():
+                _lib.check(self._stp(self.encl, int(self.encl.numel())), "stp_picard(enclave)")
+
+            if self.two_streams:
+                main = torch.cuda.current_stream()
+                self.s_hi.wait_stream(main)
+                self.s_lo.wait_stream(main)
+                with torch.cuda.stream(self.s_hi):
+                    skeleton_phase()
+                with torch.cuda.stream(self.s_lo):
+                    enclave_phase()
+                main.wait_stream(self.s_hi)
+                main.wait_stream(self.s_lo)
+            else:
+                skeleton_phase()
+                enclave_phase()
+            self._faces(nsk, F - nsk)
+            _lib.check(lib.edg_corrector(C.byref(self.native), self.order, _lib.ptr(self.table), self.ncells,
+                                         _lib.ptr(self.q_end), _lib.ptr(self.trace_q), _lib.ptr(self.trace_f),
+                                         None, _lib.ptr(self.side_face), _lib.ptr(self.outcomes),
+                                         _lib.ptr(self.edges), self.edges_per_cell, _lib.ptr(self.Qn),
+                                         _lib.ptr(self.slots), _lib.ptr(self.hmin), _lib.ptr(self.status),
+                                         _stream()), "corrector")
+        self.Q, self.Qn = self.Qn, self.Q
+
+
+class FVSolver(_Base):
+    """Patch finite-volume stepping (config 4): patches (B, m, k^3) of a
+    Cartesian patch grid, outflow boundaries."""
+
+    def __init__(self, pde: PdeDescriptor, cells_per_axis: int, k: int, cfl: float, periodic: bool = False,
+                 check_finite: bool = True, max_steps: int = 4096):
+        torch = self.torch = _torch()
+        self.lib = _lib.load()
+        if cells_per_axis % k:
+            raise ConfigError("cells per axis must be a multiple of the patch size")
+        self.pde, self.k, self.cfl = pde, k, float(cfl)
+        self.check_finite = check_finite
+        self.native = pde.native()
+        d, m = pde.dim, pde.m
+        npx = cells_per_axis // k
+        self.pmesh = CartesianMesh(npx, d, periodic)
+        self.npatches = self.pmesh.ncells
+        self.h_cell = 1.0 / cells_per_axis
+        f64 = dict(dtype=torch.float64, device="cuda")
+        self.Q = torch.zeros((self.npatches, m) + (k,) * d, **f64)
+        self.Qn = torch.zeros_like(self.Q)
+        self.nbr = torch.from_numpy(self.pmesh.nbr.copy()).cuda()
+        self.edges = torch.tensor([self.h_cell * k] * d, **f64)
+        self.hmin = torch.tensor([self.h_cell], **f64)
+        self._common_alloc(max_steps)
+
+    def set_state(self, P):
+        torch = self.torch
+        src = P if isinstance(P, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(P, dtype=np.float64))
+        self.Q.copy_(src.reshape(self.Q.shape), non_blocking=True)
+        self.steps_done = 0
+        self.status.zero_()
+        _lib.check(self.lib.edg_dt_slots_reset(_lib.ptr(self.slots), _stream()), "dt reset")
+        _lib.check(self.lib.edg_cell_speed_reduce(C.byref(self.native), 0, self.npatches, self.k ** self.pde.dim,
+                                                  _lib.ptr(self.Q), _lib.ptr(self.hmin), 0, _lib.ptr(self.slots),
+                                                  _stream()), "admissible_dt")
+
+    def state(self):
+        return self.Q
+
+    def _enqueue_step(self):
+        lib = self.lib
+        self._finalize_dt()
+        tm = self.kernel_timer
+        if tm:
+            tm.begin("fv")
+        _lib.check(lib.edg_fv_patch_step(C.byref(self.native), self.k, self.npatches, _lib.ptr(self.Q),
+                                         _lib.ptr(self.nbr), _lib.ptr(self.dt), _lib.ptr(self.edges),
+                                         _lib.ptr(self.Qn), _lib.ptr(self.slots), self.h_cell,
+                                         _lib.ptr(self.status), _stream()), "fv_patch_step")
+        if tm:
+            tm.end("fv")
+        self.Q, self.Qn = self.Qn, self.Q

@@ -1,0 +1,233 @@
+"""GPU parity of whole time steps (the Algorithm-1 path of the five configs)
+against the reference trajectories (tests/golden/traj.npz) and the oracle.
+
+Tolerance: relative L-infinity <= 1e-10 after the stated number of steps
+(BASELINE.json:north_star); FV (config 4) is bit-exact by construction."""
+import numpy as np
+import pytest
+
+from conftest import rel_linf
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def edg():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1806_07984_b200 as pkg
+    return pkg
+
+
+def _dg_solver(edg, cfg, N=None, extent=1.0, periodic=None, two_streams=True):
+    pde = edg.pde.make_pde(cfg.pde, dim=cfg.dim, **({"velocity": cfg.velocity} if cfg.pde == "advection" else {}))
+    mesh = edg.mesh.CartesianMesh(N or cfg.cells, cfg.dim, cfg.periodic if periodic is None else periodic,
+                                  extent=extent)
+    return edg.solver.DGSolver(pde, cfg.order, mesh, cfg.cfl)
+
+
+def test_cfg1_full_run_vs_reference(edg, golden_traj):
+    cfg = edg.configs.CONFIGS["cfg1"]
+    s = _dg_solver(edg, cfg)
+    s.set_state(golden_traj["cfg1_q0"])
+    s.run(cfg.steps, graph=False)
+    s.check_status()
+    Q = s.state().cpu().numpy()
+    assert rel_linf(Q, golden_traj["cfg1_q"]) <= TOL
+    assert np.array_equal(s.dt_history(), golden_traj["cfg1_dt"])
+
+
+@pytest.mark.parametrize("tag", ["cfg2p", "cfg2s", "cfg3w"])
+def test_dg_proxies_vs_reference(edg, golden_traj, tag):
+    N, dim, p, periodic, steps, cells, wlo = (int(v) for v in golden_traj[tag + "_meta"])
+    base = {"cfg2p": "cfg2", "cfg2s": "cfg2", "cfg3w": "cfg3"}[tag]
+    cfg = edg.configs.CONFIGS[base].with_(cfl=float(golden_traj[tag + "_cfl"]))
+    s = _dg_solver(edg, cfg, N=N, extent=N / cells, periodic=bool(periodic))
+    s.set_state(golden_traj[tag + "_q0"])
+    s.run(steps, graph=False)
+    s.check_status()
+    assert np.array_equal(s.iterations.cpu().numpy(), golden_traj[tag + "_its"][-1])
+    assert rel_linf(s.dt_history(), golden_traj[tag + "_dt"]) < 1e-13
+    assert rel_linf(s.state().cpu().numpy(), golden_traj[tag + "_q"]) <= TOL
+
+
+def test_fv_proxy_bitwise_vs_reference(edg, golden_traj):
+    cfg = edg.configs.CONFIGS["cfg4"]
+    s = edg.solver.FVSolver(edg.pde.euler(3), 16, 8, cfg.cfl)
+    s.set_state(golden_traj["cfg4p_q0"])
+    s.run(5, graph=False)
+    s.check_status()
+    assert np.array_equal(s.dt_history(), golden_traj["cfg4p_dt"])
+    assert np.array_equal(s.state().cpu().numpy(), golden_traj["cfg4p_q"])
+
+
+def _amr(edg, base_cells, two_streams=True, cfl=None):
+    cfg = edg.configs.CONFIGS["cfg5"].with_(cells=base_cells)
+    if cfl is not None:
+        cfg = cfg.with_(cfl=cfl)
+    mesh = edg.mesh.AdaptiveMesh(edg.configs.amr_cells(cfg), 2, True)
+    s = edg.solver.DGSolver(edg.pde.euler(2), cfg.order, mesh, cfg.cfl, two_streams=two_streams)
+    Q0 = edg.configs.initial_dg_amr(cfg, mesh.cells)
+    return cfg, mesh, s, Q0
+
+
+def test_amr_proxy_vs_reference(edg, golden_traj):
+    cfg, mesh, s, Q0 = _amr(edg, 9)
+    assert np.array_equal(Q0, golden_traj["cfg5p_q0"])
+    s.set_state(Q0)
+    s.run(3, graph=False)
+    s.check_status()
+    assert rel_linf(s.dt_history(), golden_traj["cfg5p_dt"]) < 1e-13
+    assert np.array_equal(s.iterations.cpu().numpy(), golden_traj["cfg5p_its"][-1])
+    assert rel_linf(s.state().cpu().numpy(), golden_traj["cfg5p_q"]) <= TOL
+
+
+def test_amr_schedule_variants_bitwise(edg):
+    """SPEC.md:407 variant equivalence: the two-priority-stream schedule, the
+    single-stream order and the CUDA-graph replay give identical bits."""
+    outs = []
+    for two, graph in ((True, False), (False, False), (True, True)):
+        cfg, mesh, s, Q0 = _amr(edg, 27, two_streams=two)
+        s.set_state(Q0)
+        s.run(4, graph=graph)
+        s.check_status()
+        outs.append(s.state().cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])
+
+
+def test_amr_27_vs_oracle_parity_safe(edg):
+    from oracle import drivers, ops, spacetree
+    cfg, mesh, s, Q0 = _amr(edg, 27)
+    steps = 6
+    s.set_state(Q0)
+    s.run(steps, graph=True)
+    s.check_status()
+    forest = spacetree.FaceForest(edg.configs.amr_cells(cfg), 2, True)
+    assert [c for c in forest.sfc] == mesh.cells
+    Qo, log = drivers.dg_amr_run(forest, {k: Q0[i] for i, k in enumerate(forest.sfc)}, ops.euler(2), cfg.order,
+                                 cfg.cfl, steps)
+    ref = np.stack([Qo[k] for k in forest.sfc])
+    assert rel_linf(s.dt_history(), np.array(log["dt"])) < 1e-13
+    assert rel_linf(s.state().cpu().numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("cfl,steps", [(0.2, 50), (0.9, 10)])
+def test_cfg2_27_vs_oracle(edg, cfl, steps):
+    from oracle import drivers, ops
+    cfg = edg.configs.CONFIGS["cfg2"].with_(cells=27, cfl=cfl)
+    Q0 = edg.configs.initial_dg_uniform(cfg)
+    s = _dg_solver(edg, cfg)
+    s.set_state(Q0)
+    s.run(steps, graph=True)
+    s.check_status()
+    Qo, log = drivers.dg_uniform_run(Q0, ops.euler(2), cfg.order, 27, 2, True, cfg.cfl, steps)
+    assert rel_linf(s.dt_history(), np.array(log["dt"])) < 1e-12
+    assert rel_linf(s.state().cpu().numpy(), Qo) <= TOL
+
+
+def test_cfg3_window_20_steps_vs_oracle(edg):
+    from oracle import drivers, ops
+    cfg = edg.configs.CONFIGS["cfg3"]
+    W = 8
+    Q0 = edg.configs.initial_dg_uniform(cfg, window=(12, W))
+    s = _dg_solver(edg, cfg, N=W, extent=W / cfg.cells, periodic=False)
+    s.set_state(Q0)
+    s.run(cfg.steps, graph=True)
+    s.check_status()
+    Qo, log = drivers.dg_uniform_run(Q0, ops.euler(3), cfg.order, W, 3, False, cfg.cfl, cfg.steps, h=1 / cfg.cells)
+    assert rel_linf(s.state().cpu().numpy(), Qo) <= TOL
+
+
+def test_cfg4_full_size_two_steps_bitwise(edg):
+    from oracle import drivers, ops
+    cfg = edg.configs.CONFIGS["cfg4"]
+    P0 = edg.configs.initial_fv(cfg)
+    s = edg.solver.FVSolver(edg.pde.euler(3), cfg.cells, cfg.patch, cfg.cfl)
+    s.set_state(P0)
+    s.run(2, graph=False)
+    s.check_status()
+    P, log = drivers.fv_run(P0, ops.euler(3), cfg.cells, cfg.patch, cfg.cfl, 2)
+    assert np.array_equal(s.dt_history(), np.array(log["dt"]))
+    assert np.array_equal(s.state().cpu().numpy(), P)
+
+
+def test_cfg4_32_cubed_100_steps_bitwise(edg):
+    from oracle import drivers, ops
+    cfg = edg.configs.CONFIGS["cfg4"].with_(cells=32)
+    P0 = edg.configs.initial_fv(cfg)
+    s = edg.solver.FVSolver(edg.pde.euler(3), 32, 8, cfg.cfl)
+    s.set_state(P0)
+    s.run(cfg.steps, graph=True)
+    s.check_status()
+    P, log = drivers.fv_run(P0, ops.euler(3), 32, 8, cfg.cfl, cfg.steps)
+    assert np.array_equal(s.state().cpu().numpy(), P)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_full_size_step_sampled_cells_vs_oracle(edg, name):
+    """Full-size configs: one GPU step; the predictor of a random cell sample
+    is checked against the per-cell oracle (cell-local => size independent),
+    and the corrector of those cells is re-evaluated by the oracle from the
+    GPU's neighbour traces."""
+    import torch
+    from oracle import ops
+    cfg = edg.configs.CONFIGS[name]
+    Q0 = edg.configs.initial_dg_uniform(cfg)
+    s = _dg_solver(edg, cfg)
+    s.set_state(Q0)
+    s.step()
+    s.check_status()
+    torch.cuda.synchronize()
+    dt = float(s.dt_history()[0])
+    pde, b = ops.euler(cfg.dim), ops.basis_for(cfg.order)
+    h = 1.0 / cfg.cells
+    assert dt == pytest.approx(ops.stable_dt(((h, Q0[c]) for c in range(0, Q0.shape[0], 97)), pde, cfg.order,
+                                             cfg.cfl, cfg.dim), rel=0.5)
+    rng = np.random.default_rng(1)
+    sample = rng.choice(Q0.shape[0], 48, replace=False)
+    tq = s.trace_q.cpu().numpy()
+    tf = s.trace_f.cpu().numpy()
+    qe = s.q_end.cpu().numpy()
+    its = s.iterations.cpu().numpy()
+    Qn = s.state().cpu().numpy()
+    nbr = s.mesh.nbr
+    keys = [(a, si) for a in range(cfg.dim) for si in (0, 1)]
+    for c in sample:
+        st = ops.predictor_picard(Q0[c], pde, dt, b, (h,) * cfg.dim)
+        assert st.iterations == its[c]
+        assert rel_linf(qe[c], st.q_end) < 1e-12
+        for j, k in enumerate(keys):
+            assert rel_linf(tf[c, j], st.trace_f[k]) < 1e-12
+            assert rel_linf(tq[c, j], st.trace_q[k]) < 1e-12
+        outc = {}
+        for j, (a, si) in enumerate(keys):
+            nb = nbr[c, j]
+            mine = tq[c, j]
+            theirs = tq[nb, 2 * a + (1 - si)] if nb >= 0 else mine
+            lo, hi = (mine, theirs) if si == 1 else (theirs, mine)
+            outc[(a, si)] = ops.rusanov(lo, hi, pde, a)
+        gstore = ops.Store(None, qe[c], None, {k: tf[c, j] for j, k in enumerate(keys)})
+        assert np.array_equal(ops.correct(gstore, outc, b, (h,) * cfg.dim), Qn[c])
+
+
+def test_cfg2_full_size_conservation_and_constant_state(edg):
+    import torch
+    cfg = edg.configs.CONFIGS["cfg2"]
+    s = _dg_solver(edg, cfg)
+    Q0 = edg.configs.initial_dg_uniform(cfg)
+    s.set_state(Q0)
+    b = edg.basis.get_basis(cfg.order)
+    w2 = torch.from_numpy(np.outer(b.weights, b.weights)).cuda()
+    m0 = (s.state() * w2).sum(dim=(0, 2, 3))
+    s.run(4, graph=True)
+    s.check_status()
+    m1 = (s.state() * w2).sum(dim=(0, 2, 3))
+    assert float(((m1 - m0).abs() / m0.abs()).max()) < 1e-12
+    # a constant state is a fixed point
+    Qc = np.zeros_like(Q0)
+    Qc[:, 0], Qc[:, 1], Qc[:, 2], Qc[:, 3] = 1.0, 0.3, -0.2, 2.5
+    s.set_state(Qc)
+    s.run(2, graph=False)
+    assert rel_linf(s.state().cpu().numpy(), Qc) < 1e-13
