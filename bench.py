@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--cfl", type=float, default=None, help="override the config's CFL safety")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variant", action="store_true", help="skip the parity-safe CFL 0.2 variant line item")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -302,19 +303,16 @@ def run_reference(args, cfg):
 
 # ------------------------------------------------------------------ ours --
 
-def run_ours(args, cfg):
+def measure_device(cfg, steps, warmup, ws, dist, dev, peak64, local):
+    """Kernel-resident timing of `steps` consecutive time steps after `warmup`
+    steps from the initial state; per-kernel CUDA events on the launching
+    stream give the roofline numerators."""
     import torch
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist = dist_init(ws, "nccl")
     from paper_1806_07984_b200 import solver as S
-
-    peak64 = fp64_peak_tflops()
     solver, Q0, ncells = build_solver(cfg)
     dof = cf.dof_count(cfg, ncells)
     solver.set_state(Q0)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         solver.step()
     torch.cuda.synchronize()
     its0 = int(solver.iter_total.item()) if hasattr(solver, "iter_total") else 0
@@ -327,7 +325,7 @@ def run_ours(args, cfg):
     stop = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         start.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             solver.step()
         stop.record()
         torch.cuda.synchronize()
@@ -336,88 +334,104 @@ def run_ours(args, cfg):
     solver.kernel_timer = None
     ms = start.elapsed_time(stop)
     ms_max = max_over_ranks(dist, ms, dev)
-    value = dof * args.steps * ws / (ms_max * 1e-3)
     tot = timer.totals_ms()
     status = solver.status.cpu().numpy()
     hbm = measured_peaks().get("hbm_gbs")
-
-    kernels = {}
-    launches = 0
+    kernels, iters_mean = {}, None
     if cfg.kind == "fv":
         n_fv, ms_fv = tot["fv"]
-        launches = args.steps * 2
+        launches = steps * 2
         cells = cfg.cells ** 3
-        byt = costs.fv_cell_bytes(cfg.m) * cells
-        ach = byt / (ms_fv / n_fv * 1e-3) / 1e9
+        ach = costs.fv_cell_bytes(cfg.m) * cells / (ms_fv / n_fv * 1e-3) / 1e9
         kernels["fv_patch"] = {"ms_per_launch": ms_fv / n_fv, "bound": "hbm", "achieved": ach, "unit": "GB/s",
                                "peak": hbm, "frac": ach / hbm if hbm else None,
-                               "gflops": costs.fv_cell_flops("euler") * cells / (ms_fv / n_fv * 1e-3) / 1e9}
+                               "fp64_tflops": costs.fv_cell_flops("euler") * cells / (ms_fv / n_fv * 1e-3) / 1e12}
         roof = dict(kernels["fv_patch"], kernel="fv_patch")
-        iters_mean = None
-    elif "stp" not in tot:      # adaptive schedule: kernels run on two streams, no per-kernel events
+    elif "stp" not in tot:      # adaptive schedule: two streams, no per-kernel events
         its = int(solver.iter_total.item()) - its0
-        iters_mean = its / (args.steps * ncells)
-        launches = args.steps * 7
+        iters_mean = its / (steps * ncells)
+        launches = steps * 7
         roof = {"bound": "fp64", "achieved": None, "peak": peak64, "unit": "TFLOP/s", "frac": None,
                 "kernel": "stp_picard"}
     else:
         d, n, m = cfg.dim, cfg.n, cfg.m
         its = int(solver.iter_total.item()) - its0
-        iters_mean = its / (args.steps * ncells)
+        iters_mean = its / (steps * ncells)
         n_stp, ms_stp = tot["stp"]
-        flops = its * costs.stp_iter_flops(cfg.pde, d, n, m) + args.steps * ncells * costs.stp_epilogue_flops(
+        flops = its * costs.stp_iter_flops(cfg.pde, d, n, m) + steps * ncells * costs.stp_epilogue_flops(
             cfg.pde, d, n, m)
         ach = flops / (ms_stp * 1e-3) / 1e12
         kernels["stp_picard"] = {"ms_per_launch": ms_stp / n_stp, "bound": "fp64", "achieved": ach,
                                  "unit": "TFLOP/s", "peak": peak64, "frac": ach / peak64,
-                                 "hbm_gbs": costs.stp_bytes(d, n, m) * ncells / (ms_stp / n_stp * 1e-3) / 1e9}
+                                 "hbm_gbs": costs.stp_bytes(d, n, m) * ncells / (ms_stp / n_stp * 1e-3) / 1e9,
+                                 "flops_per_launch": flops / n_stp}
         n_c, ms_c = tot["corrector"]
         cb = costs.corrector_bytes(d, n, m) * ncells / (ms_c / n_c * 1e-3) / 1e9
         kernels["corrector_fused"] = {"ms_per_launch": ms_c / n_c, "bound": "hbm", "achieved": cb, "unit": "GB/s",
                                       "peak": hbm, "frac": cb / hbm if hbm else None}
-        launches = args.steps * 3
+        launches = steps * 3
         roof = dict(kernels["stp_picard"], kernel="stp_picard")
-    share = {k: v["ms_per_launch"] * args.steps / ms for k, v in kernels.items()}
+    share = {k: v["ms_per_launch"] * steps / ms for k, v in kernels.items()}
+    return dict(solver=solver, Q0=Q0, ncells=ncells, dof=dof, ms=ms_max, value=dof * steps * ws / (ms_max * 1e-3),
+                kernels=kernels, roof=roof, share=share, iters_mean=iters_mean, launches=launches,
+                clocks=clocks.summary(), nonfinite_cells=int(status[1]), first_nonfinite_step=int(status[3]) or None)
 
+
+def run_ours(args, cfg):
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = dist_init(ws, "nccl")
+    peak64 = fp64_peak_tflops()
+    r = measure_device(cfg, args.steps, args.warmup, ws, dist, dev, peak64, local)
+    roof = r["roof"]
     traffic = None
     try:
         tr = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
         traffic = tr.get(cfg.name, {}).get(roof["kernel"])
     except (OSError, ValueError):
         pass
-
+    variant = None
+    if cfg.kind != "fv" and cfg.cfl > 0.2 and not args.no_variant:
+        v = measure_device(cfg.with_(cfl=0.2), args.steps, args.warmup, ws, dist, dev, peak64, local)
+        variant = {"cfl_safety": 0.2, "why": "parity-safe CFL (SURVEY.md section 7 hard part 1)",
+                   "value": v["value"], "ms_per_step": v["ms"] / args.steps,
+                   "picard_iterations_mean": v["iters_mean"], "nonfinite_cells": v["nonfinite_cells"],
+                   "roofline_frac": v["roof"]["frac"], "kernels": v["kernels"]}
+        del v
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(solver, Q0, dof, args.steps, ws, dist, dev)
-
+        e2e = measure_e2e(r["solver"], r["Q0"], r["dof"], args.steps, ws, dist, dev)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and cfg.kind == "dg":
         rates, cores, sample = cpu_port_rate(cfg.name, args.cfl, args.cpu_seconds, steps=1)
         cpu = {"value": rates[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
                "cpu": cpu_model()}
-
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs.py)",
-            "config": {"workload": workload_name(cfg), "cells": ncells, "dof": dof, "cfl_safety": cfg.cfl,
+            "config": {"workload": workload_name(cfg), "cells": r["ncells"], "dof": r["dof"], "cfl_safety": cfg.cfl,
                        "parallelism": f"replicas x{ws} (the path does not shard in this tier)",
                        "steps_from_ic": f"{args.warmup + 1}..{args.warmup + args.steps}",
                        "l2": "working set > 126 MB L2 (state + predictor buffers), no flush",
-                       "picard_iterations_mean": iters_mean,
-                       "nonfinite_cell_steps": int(status[1])},
+                       "picard_iterations_mean": r["iters_mean"],
+                       "nonfinite_cell_results": r["nonfinite_cells"],
+                       "first_nonfinite_step": r["first_nonfinite_step"]},
             "roofline": {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
                          "unit": roof["unit"], "frac": roof["frac"], "traffic": traffic,
                          "kernel": roof["kernel"],
                          "peak_source": ("fp64: DFMA probe measured in this run (MEASURED_PEAKS.json has no FP64)"
                                          if roof["bound"] == "fp64" else "MEASURED_PEAKS.json hbm_gbs")},
-            "kernels": kernels, "kernel_share_of_step": share,
+            "kernels": r["kernels"], "kernel_share_of_step": r["share"],
             "fp64_peak_tflops_measured": peak64,
-            "gpu_launches": launches,
-            "clocks": clocks.summary(),
+            "gpu_launches": r["launches"],
+            "clocks": r["clocks"],
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity_safe_variant": variant,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -121,7 +121,8 @@ int edg_corrector(const edg_pde* pde, int32_t order, const double* basis_dev, in
  * dt_hist_dev is non-null, dt_hist_dev[step] -- or, for step < 0,
  * dt_hist_dev[status_dev[2]++] bounded by -step), re-arms the slots; no
  * positive speed -> dt = NaN and status_dev[0] |= 1 (EDG_ERR_NO_SPEED).
- * status_dev layout: [0] flags, [1] non-finite cells, [2] step counter. */
+ * status_dev layout: [0] flags, [1] non-finite cell results (cumulative),
+ * [2] step counter, [3] first step (1-based) whose result was non-finite. */
 int edg_cell_speed_reduce(const edg_pde* pde, int32_t order, int32_t ncells, int32_t npts,
                           const double* q_dev, const double* hmin_dev, int32_t h_per_cell,
                           unsigned long long* dt_slots_dev, void* stream);

@@ -88,6 +88,8 @@ static __global__ void dt_finalize_kernel(unsigned long long* slots, double cfl,
       v = __dmul_rn(cfl, __longlong_as_double((long long)s[0]));
     }
     *dt = v;
+    // status[3]: 1-based index of the first step whose result was non-finite
+    if (status && status[1] != 0u && status[3] == 0u) status[3] = status[2];
     if (hist) {
       // step >= 0: explicit slot; step < 0: device counter status[2] with
       // capacity -step (graph-replay friendly)

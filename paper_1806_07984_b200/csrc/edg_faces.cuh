@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
   const bool has_cell = slot < CPB && cell < A.ncells;
 
   if (tid < CPB * DIM) sLam[tid] = 0ull;
+  if (tid < CPB) sBest[tid] = 0ull;   // doubles as the per-cell non-finite flag until phase 3
   // lift vectors v[a][s][i] = (sign * l_i(s)) / (w_i * h_a)   (kernels.py:190-191)
   if (has_cell) {
     const double* e = A.edges + (A.edges_per_cell ? (size_t)cell * DIM : 0);
@@ -161,7 +162,13 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       for (int a = 0; a < DIM; ++a) atomicMax(sLam + slot * DIM + a, maxkey(P::lam(qn, pr, a, A.pp)));
     }
   }
-  if (A.status && has_cell && !finite) atomicAdd(A.status + 1, 1u);
+  // per-cell non-finite flag (counted once per cell)
+  if (has_cell && !finite) atomicOr(reinterpret_cast<unsigned int*>(sBest + slot), 1u);
+  if (A.dt_slots || A.status) {
+    __syncthreads();
+    if (A.status && tid < CPB && (reinterpret_cast<unsigned int*>(sBest + tid)[0] & 1u))
+      atomicAdd(A.status + 1, 1u);
+  }
   if (A.dt_slots) {
     __syncthreads();
     // phase 3: per-cell lambda (python max over axes) -> candidate -> slot min
