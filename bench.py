@@ -369,7 +369,7 @@ def measure_device(cfg, steps, warmup, ws, dist, dev, peak64, local):
         cb = costs.corrector_bytes(d, n, m) * ncells / (ms_c / n_c * 1e-3) / 1e9
         kernels["corrector_fused"] = {"ms_per_launch": ms_c / n_c, "bound": "hbm", "achieved": cb, "unit": "GB/s",
                                       "peak": hbm, "frac": cb / hbm if hbm else None}
-        launches = steps * 3
+        launches = steps * 6
         roof = dict(kernels["stp_picard"], kernel="stp_picard")
     share = {k: v["ms_per_launch"] * steps / ms for k, v in kernels.items()}
     return dict(solver=solver, Q0=Q0, ncells=ncells, dof=dof, ms=ms_max, value=dof * steps * ws / (ms_max * 1e-3),

@@ -82,6 +82,12 @@ int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev,
                    double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev,
                    unsigned long long* iter_total_dev, void* stream);
 
+/* Work ordering for the next predictor launch: order_dev = the cells sorted
+ * by descending Picard count (counting sort, 3 small kernels).  scratch_dev:
+ * 128 int32, zero-initialised once by the caller. */
+int edg_order_by_iterations(int32_t ncells, const int32_t* iterations_dev, int32_t* order_dev,
+                            int32_t* scratch_dev, void* stream);
+
 /* ---- project_to_faces (kernels.py:73-79): vol (C,m,n^d) -> (C,2d,m,n^(d-1)) */
 int edg_project_to_faces(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t ncells,
                          const double* vol_dev, double* traces_dev, void* stream);

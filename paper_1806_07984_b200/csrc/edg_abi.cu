@@ -372,6 +372,19 @@ static __global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, in
 
 extern "C" {
 
+int edg_order_by_iterations(int32_t ncells, const int32_t* iterations_dev, int32_t* order_dev,
+                            int32_t* scratch_dev, void* stream) {
+  if (ncells <= 0) return EDG_OK;
+  const cudaStream_t st = (cudaStream_t)stream;
+  int32_t* hist = scratch_dev;
+  int32_t* offs = scratch_dev + ORDER_BINS;
+  const unsigned blocks = (unsigned)((ncells + 255) / 256);
+  order_hist_kernel<<<blocks, 256, 0, st>>>(ncells, iterations_dev, hist);
+  order_scan_kernel<<<1, 32, 0, st>>>(hist, offs);
+  order_scatter_kernel<<<blocks, 256, 0, st>>>(ncells, iterations_dev, offs, order_dev);
+  return cuda_status(check_launch());
+}
+
 int edg_probe_fp64(double* sink_dev, int32_t blocks, int32_t iters, void* stream) {
   fp64_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink_dev, iters);
   return cuda_status(check_launch());

@@ -101,6 +101,53 @@ struct Pde<EDG_PDE_EULER, DIM> {
   }
 };
 
+// ------------------------------------------------- fast flux (STP only) --
+// Inside the Picard iteration the result is already a non-associative fp64
+// contraction (not bit-comparable with OpenBLAS), so the flux there may use a
+// branch-free reciprocal (MUFU seed + two Newton steps, <= 1 ulp) and FMA
+// contraction.  Riemann, corrector, FV and dt keep the exact versions above.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+template <int KIND, int DIM>
+struct FastFlux {
+  // all-axes flux F[a][k] of one state
+  template <int M>
+  __device__ __forceinline__ static void all(const double* q, const PdeParams& pp, double (&F)[DIM][M]) {
+    using P = Pde<KIND, DIM>;
+    const auto pr = P::parts(q, pp);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) P::flux(q, pr, a, pp, F[a]);
+  }
+};
+
+template <int DIM>
+struct FastFlux<EDG_PDE_EULER, DIM> {
+  template <int M>
+  __device__ __forceinline__ static void all(const double* q, const PdeParams& pp, double (&F)[DIM][M]) {
+    const double inv = fast_rcp(q[0]);
+    double ke = q[1] * q[1];
+#pragma unroll
+    for (int i = 1; i < DIM; ++i) ke = fma(q[1 + i], q[1 + i], ke);
+    const double p = pp.gm1 * fma(-0.5 * ke, inv, q[1 + DIM]);
+    const double ep = q[1 + DIM] + p;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const double u = q[1 + a] * inv;
+      F[a][0] = q[1 + a];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) F[a][1 + i] = (i == a) ? fma(q[1 + i], u, p) : q[1 + i] * u;
+      F[a][1 + DIM] = ep * u;
+    }
+  }
+};
+
 // np.maximum semantics: NaN if either operand is NaN.
 __device__ __forceinline__ double nan_max(double a, double b) {
   if (a != a) return a;

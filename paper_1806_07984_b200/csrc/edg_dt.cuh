@@ -103,6 +103,50 @@ static __global__ void dt_finalize_kernel(unsigned long long* slots, double cfl,
   }
 }
 
+// ---------------------------------------- Picard-count ordering of cells --
+// Counting sort of the cells by their last Picard iteration count, so that a
+// CTA of the next predictor launch holds cells that will iterate alike (the
+// CTA runs until its slowest cell converges).  Order inside a bucket is not
+// deterministic; results are, because cells are independent.
+constexpr int ORDER_BINS = 64;
+
+static __global__ void order_hist_kernel(int n, const int32_t* its, int32_t* hist) {
+  __shared__ int32_t h[ORDER_BINS];
+  for (int i = threadIdx.x; i < ORDER_BINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) atomicAdd(&h[min(max(its[c], 0), ORDER_BINS - 1)], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < ORDER_BINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+static __global__ void order_scan_kernel(int32_t* hist, int32_t* offs) {
+  // descending iteration count first: the heaviest CTAs start earliest
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = ORDER_BINS - 1; b >= 0; --b) {
+      offs[b] = acc;
+      acc += hist[b];
+      hist[b] = 0;
+    }
+  }
+}
+
+static __global__ void order_scatter_kernel(int n, const int32_t* its, int32_t* offs, int32_t* order) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ok = c < n;
+  const int b = ok ? min(max(its[c], 0), ORDER_BINS - 1) : -1;
+  // warp-aggregated slot reservation per bucket
+  const unsigned peers = __match_any_sync(0xffffffffu, b);
+  const int leader = __ffs(peers) - 1;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (ok && lane == leader) base = atomicAdd(&offs[b], __popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (ok) order[base + __popc(peers & ((1u << lane) - 1u))] = c;
+}
+
 template <int KIND, int DIM>
 __global__ void riemann_batch_kernel(int nfaces, int npts, const double* lo, const double* hi, int axis, int sign,
                                      double* out, PdeParams pp) {

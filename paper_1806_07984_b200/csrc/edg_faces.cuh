@@ -74,6 +74,11 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
 
   if (tid < CPB * DIM) sLam[tid] = 0ull;
   if (tid < CPB) sBest[tid] = 0ull;   // doubles as the per-cell non-finite flag until phase 3
+  // q_end of this node, prefetched so its loads overlap the face gathers
+  double qn[M];
+  const size_t cb = (size_t)cell * M * NPC;
+#pragma unroll
+  for (int k = 0; k < M; ++k) qn[k] = has_cell ? __ldg(A.q_end + cb + (size_t)k * NPC + node) : 0.0;
   // lift vectors v[a][s][i] = (sign * l_i(s)) / (w_i * h_a)   (kernels.py:190-191)
   if (has_cell) {
     const double* e = A.edges + (A.edges_per_cell ? (size_t)cell * DIM : 0);
@@ -126,7 +131,6 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
   }
   __syncthreads();
   // phase 2: Q = q_end - sum v (x) jump, reference (a, s) order
-  double qn[M];
   bool finite = true;
   if (has_cell) {
     int ix[DIM];
@@ -136,9 +140,6 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       ix[a] = t % N;
       t /= N;
     }
-    const size_t cb = (size_t)cell * M * NPC;
-#pragma unroll
-    for (int k = 0; k < M; ++k) qn[k] = A.q_end[cb + (size_t)k * NPC + node];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
       const int st = ipow(N, DIM - 1 - a);

@@ -1,17 +1,19 @@
 // Patch finite-volume update -- replaces kernels.py:225-264.
 //
-// One CTA per k^d patch.  The patch and its 2d face halos (a neighbour
-// patch's boundary layer, kernels.py:256-264, or the own layer at an outflow
-// boundary) are staged once in shared memory as a (k+2)^d block, together
-// with the state-only parts of the flux (1/rho and p for Euler).  Each thread
-// owns one volume and applies, in the reference order a = 0..d-1,
+// One CTA per k^d patch (256 threads; two CTAs resident per SM so one CTA's
+// loads overlap the other's arithmetic).  The patch and its 2d face halos (a
+// neighbour patch's boundary layer, kernels.py:256-264, or the own layer at
+// an outflow boundary) are staged once in shared memory as a (k+2)^d block,
+// together with the state-only parts of the flux (1/rho, p and the sound
+// speed for Euler), evaluated once per state.  Then, axis by axis in the
+// reference order a = 0..d-1, every unique interface flux of the patch is
+// evaluated once into a shared buffer and each volume applies
 //     out -= (dt / dx_a) * (F_{i+1/2} - F_{i-1/2})
-// with every interface flux evaluated by the bit-exact Rusanov of
-// edg_common.cuh from the ORIGINAL states (unsplit, kernels.py:240-252); an
-// interface shared by two threads is evaluated twice with identical inputs,
-// hence identically.  The next step's admissible-dt candidate of the patch
-// (lambda over its volumes, kernels.py:267-281 with order 0) is fused into
-// the epilogue.
+// from the ORIGINAL states (unsplit, kernels.py:240-252).  Every operation is
+// the non-contracted round-to-nearest sequence of edg_common.cuh, so the
+// result is bit-identical to the reference.  The next step's admissible-dt
+// candidate of the patch (lambda over its volumes, kernels.py:267-281 with
+// order 0) is fused into the epilogue.
 #pragma once
 #include "edg_common.cuh"
 
@@ -35,77 +37,84 @@ template <int DIM, int K>
 struct FvCfg {
   static constexpr int NC = ipow(K, DIM);
   static constexpr int NE = ipow(K + 2, DIM);
-  static constexpr int THREADS = NC >= 512 ? 512 : ((NC + 31) / 32) * 32;
+  static constexpr int NL = ipow(K, DIM - 1);           // cells per layer / pencils per axis
+  static constexpr int NI = (K + 1) * NL;               // interfaces per axis
+  static constexpr int THREADS = NC >= 256 ? 256 : ((NC + 31) / 32) * 32;
+  static constexpr int CPT = (NC + THREADS - 1) / THREADS;   // volumes per thread
 };
 
 template <int KIND, int DIM, int K>
 struct FvSmem {
   static constexpr int M = Pde<KIND, DIM>::M;
-  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? 2 : 0;
-  static constexpr size_t BYTES =
-      sizeof(double) * FvCfg<DIM, K>::NE * (M + NPARTS) + sizeof(unsigned long long) * DIM;
+  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? 3 : 0;
+  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + FvCfg<DIM, K>::NI * M) +
+                                  sizeof(unsigned long long) * DIM;
 };
 
-// Rusanov with precomputed state parts (same arithmetic as edg::rusanov).
-template <int KIND, int DIM>
-__device__ __forceinline__ void rusanov_pp(const double* lo, const typename Pde<KIND, DIM>::Parts& pl,
-                                           const double* hi, const typename Pde<KIND, DIM>::Parts& ph, int a,
-                                           const PdeParams& pp, double* out) {
-  using P = Pde<KIND, DIM>;
-  constexpr int M = P::M;
-  const double lam = nan_max(P::lam(lo, pl, a, pp), P::lam(hi, ph, a, pp));
-  double fl[M], fh[M];
-  P::flux(lo, pl, a, pp, fl);
-  P::flux(hi, ph, a, pp, fh);
-  const double hl = __dmul_rn(0.5, lam);
-#pragma unroll
-  for (int k = 0; k < M; ++k)
-    out[k] = __dsub_rn(__dmul_rn(0.5, __dadd_rn(fl[k], fh[k])), __dmul_rn(hl, __dsub_rn(hi[k], lo[k])));
-}
-
 template <int KIND, int DIM, int K>
-__global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS) fv_patch_kernel(const FvArgs A) {
+__global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(const FvArgs A) {
   using P = Pde<KIND, DIM>;
   using Cf = FvCfg<DIM, K>;
   constexpr int M = P::M;
-  constexpr int NC = Cf::NC, NE = Cf::NE, KE = K + 2;
-  constexpr int NL = ipow(K, DIM - 1);
+  constexpr int NC = Cf::NC, NE = Cf::NE, NL = Cf::NL, NI = Cf::NI, KE = K + 2;
+  constexpr int THREADS = Cf::THREADS, CPT = Cf::CPT;
   constexpr bool EULER = KIND == EDG_PDE_EULER;
 
   extern __shared__ __align__(16) double smem[];
-  double* sQ = smem;                          // [M][NE]
-  double* sInv = sQ + M * NE;                 // [NE] (Euler)
-  double* sP = sInv + (EULER ? NE : 0);       // [NE] (Euler)
-  unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sQ + NE * (M + (EULER ? 2 : 0)));
+  double* sQ = smem;                               // [M][NE]
+  double* sInv = sQ + M * NE;                      // [NE] (Euler)
+  double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler)
+  double* sC = sP + (EULER ? NE : 0);              // [NE] (Euler) sound speed
+  double* sFl = sC + (EULER ? NE : 0);             // [M][NI] interface fluxes of one axis
+  unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sFl + M * NI);
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
   if (tid < DIM) sLam[tid] = 0ull;
   const double* src = A.patch + (size_t)b * M * NC;
 
-  auto ext_index = [](const int* e) {
-    int idx = 0;
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) idx = idx * KE + e[a];
-    return idx;
-  };
-  // interior
-  for (int i = tid; i < M * NC; i += blockDim.x) {
-    const int k = i / NC, c = i - k * NC;
-    int e[DIM], t = c;
+  // ext index of a cell index (row-major, last axis fastest) shifted by +1
+  auto ext_of_cell = [](int c) {
+    int e = 0, mul = 1;
 #pragma unroll
     for (int a = DIM - 1; a >= 0; --a) {
-      e[a] = t % K + 1;
-      t /= K;
+      e += (c % K + 1) * mul;
+      c /= K;
+      mul *= KE;
     }
-    sQ[k * NE + ext_index(e)] = src[i];
+    return e;
+  };
+
+  // ---- stage interior + halos (all loads issued before the stores) ----
+  {
+    constexpr int NLD = (M * NC + THREADS - 1) / THREADS;
+    double v[NLD];
+#pragma unroll
+    for (int i = 0; i < NLD; ++i) {
+      const int g = tid + i * THREADS;
+      v[i] = g < M * NC ? __ldg(src + g) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < NLD; ++i) {
+      const int g = tid + i * THREADS;
+      if (g < M * NC) {
+        const int k = g / NC, c = g - k * NC;
+        sQ[k * NE + ext_of_cell(c)] = v[i];
+      }
+    }
   }
-  // face halos: layer (a, s) at ext index 0 / K+1 along a
-  for (int i = tid; i < 2 * DIM * M * NL; i += blockDim.x) {
+  for (int i = tid; i < 2 * DIM * M * NL; i += THREADS) {
     const int fs = i / (M * NL);
     const int r = i - fs * M * NL;
     const int k = r / NL, f = r - k * NL;
     const int a = fs >> 1, s = fs & 1;
+    int e[DIM], t = f;
+#pragma unroll
+    for (int ax = DIM - 1; ax >= 0; --ax) {
+      if (ax == a) continue;
+      e[ax] = t % K;
+      t /= K;
+    }
     double v;
     if (A.halos) {
       v = A.halos[(size_t)b * 2 * DIM * M * NL + i];
@@ -113,92 +122,146 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS) fv_patch_kernel(const 
       const int nb = A.nbr[(size_t)b * 2 * DIM + fs];
       // neighbour below (s=0) contributes its last layer, above its first;
       // outflow (-1): own layer on that side
-      const int layer = nb >= 0 ? (s == 0 ? K - 1 : 0) : (s == 0 ? 0 : K - 1);
-      const int pb = nb >= 0 ? nb : b;
-      int e[DIM], t = f;
-      // f enumerates the non-a axes in order
-#pragma unroll
-      for (int ax = DIM - 1; ax >= 0; --ax) {
-        if (ax == a) continue;
-        e[ax] = t % K;
-        t /= K;
-      }
-      e[a] = layer;
+      e[a] = nb >= 0 ? (s == 0 ? K - 1 : 0) : (s == 0 ? 0 : K - 1);
       int c = 0;
 #pragma unroll
       for (int ax = 0; ax < DIM; ++ax) c = c * K + e[ax];
-      v = A.patch[((size_t)pb * M + k) * NC + c];
+      v = __ldg(A.patch + ((size_t)(nb >= 0 ? nb : b) * M + k) * NC + c);
     }
-    int e[DIM], t = f;
+    int x = 0;
 #pragma unroll
-    for (int ax = DIM - 1; ax >= 0; --ax) {
-      if (ax == a) continue;
-      e[ax] = t % K + 1;
-      t /= K;
-    }
-    e[a] = s ? K + 1 : 0;
-    sQ[k * NE + ext_index(e)] = v;
+    for (int ax = 0; ax < DIM; ++ax) x = x * KE + (ax == a ? (s ? K + 1 : 0) : e[ax] + 1);
+    sQ[k * NE + x] = v;
   }
   __syncthreads();
+  // ---- state parts once per staged state (Euler: 1/rho, p, c) ----
   if constexpr (EULER) {
-    for (int i = tid; i < NE; i += blockDim.x) {
+    for (int i = tid; i < NE; i += THREADS) {
+      // skip the unused edge / corner points of the extended block
+      int t = i, outside = 0;
+#pragma unroll
+      for (int ax = 0; ax < DIM; ++ax) {
+        const int e = t % KE;
+        t /= KE;
+        outside += (e == 0 || e == K + 1);
+      }
+      if (outside > 1) continue;
       double q[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) q[k] = sQ[k * NE + i];
       const auto pr = P::parts(q, A.pp);
       sInv[i] = pr.inv;
       sP[i] = pr.p;
+      sC[i] = __dsqrt_rn(__dmul_rn(__dmul_rn(A.pp.gamma, pr.p), pr.inv));
+    }
+  }
+  const double dt = *A.dt;
+
+  // volumes owned by this thread, updated in registers across the axes
+  double o[CPT][M];
+  int me[CPT];
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int c = tid + j * THREADS;
+    me[j] = c < NC ? ext_of_cell(c) : 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < CPT; ++j)
+#pragma unroll
+    for (int k = 0; k < M; ++k) o[j][k] = sQ[k * NE + me[j]];
+
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    const double coef = __ddiv_rn(dt, __ddiv_rn(A.edges[a], (double)K));
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int st = ipow(KE, DIM - 1 - a);
+    // interfaces i = 0..K along a for every pencil p (the other axes)
+    for (int it = tid; it < NI; it += THREADS) {
+      const int i = it / NL, pcl = it - i * NL;
+      // ext index of the state below the interface: index i along a, pencil +1 elsewhere
+      int t = pcl, x = 0, mul = 1;
+#pragma unroll
+      for (int ax = DIM - 1; ax >= 0; --ax) {
+        int e;
+        if (ax == a) {
+          e = i;
+        } else {
+          e = t % K + 1;
+          t /= K;
+        }
+        x += e * mul;
+        mul *= KE;
+      }
+      const int xl = x, xh = x + st;
+      double ql[M], qh[M], f[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        ql[k] = sQ[k * NE + xl];
+        qh[k] = sQ[k * NE + xh];
+      }
+      if constexpr (EULER) {
+        const typename P::Parts pl{sInv[xl], sP[xl]}, ph{sInv[xh], sP[xh]};
+        const double ul = __dmul_rn(ql[1 + a], pl.inv), uh = __dmul_rn(qh[1 + a], ph.inv);
+        const double lam = nan_max(__dadd_rn(fabs(ul), sC[xl]), __dadd_rn(fabs(uh), sC[xh]));
+        double fl[M], fh[M];
+        P::flux(ql, pl, a, A.pp, fl);
+        P::flux(qh, ph, a, A.pp, fh);
+        const double hl = __dmul_rn(0.5, lam);
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          f[k] = __dsub_rn(__dmul_rn(0.5, __dadd_rn(fl[k], fh[k])), __dmul_rn(hl, __dsub_rn(qh[k], ql[k])));
+      } else {
+        rusanov<KIND, DIM>(ql, qh, a, 1, A.pp, f);
+      }
+#pragma unroll
+      for (int k = 0; k < M; ++k) sFl[k * NI + it] = f[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = tid + j * THREADS;
+      if (c < NC) {
+        // cell index along a and its pencil (the other axes in order)
+        int t = c, ia = 0, pcl = 0, mul = 1;
+#pragma unroll
+        for (int ax = DIM - 1; ax >= 0; --ax) {
+          const int e = t % K;
+          t /= K;
+          if (ax == a) {
+            ia = e;
+          } else {
+            pcl += e * mul;
+            mul *= K;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          o[j][k] = __dsub_rn(o[j][k],
+                              __dmul_rn(coef, __dsub_rn(sFl[k * NI + (ia + 1) * NL + pcl], sFl[k * NI + ia * NL + pcl])));
+      }
     }
     __syncthreads();
   }
-  const double dt = *A.dt;
-  double coef[DIM];
-#pragma unroll
-  for (int a = 0; a < DIM; ++a) coef[a] = __ddiv_rn(dt, __ddiv_rn(A.edges[a], (double)K));
 
-  for (int c = tid; c < NC; c += blockDim.x) {
-    int e[DIM], t = c;
+  // ---- write back, non-finite count, next-step dt candidate ----
 #pragma unroll
-    for (int a = DIM - 1; a >= 0; --a) {
-      e[a] = t % K + 1;
-      t /= K;
-    }
-    const int me = ext_index(e);
-    double q[M], o[M];
-#pragma unroll
-    for (int k = 0; k < M; ++k) o[k] = q[k] = sQ[k * NE + me];
-    typename P::Parts pm{};
-    if constexpr (EULER) pm = {sInv[me], sP[me]};
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-      const int st = ipow(KE, DIM - 1 - a);
-      double ql[M], qh[M], fl[M], fh[M];
+  for (int j = 0; j < CPT; ++j) {
+    const int c = tid + j * THREADS;
+    if (c < NC) {
+      bool finite = true;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        ql[k] = sQ[k * NE + me - st];
-        qh[k] = sQ[k * NE + me + st];
+        A.out[((size_t)b * M + k) * NC + c] = o[j][k];
+        finite = finite && (fabs(o[j][k]) <= 1.7976931348623157e308);
       }
-      typename P::Parts plo{}, phi{};
-      if constexpr (EULER) {
-        plo = {sInv[me - st], sP[me - st]};
-        phi = {sInv[me + st], sP[me + st]};
+      if (A.status && !finite) atomicAdd(A.status + 1, 1u);
+      if (A.dt_slots) {
+        const auto pr = P::parts(o[j], A.pp);
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) atomicMax(sLam + a, maxkey(P::lam(o[j], pr, a, A.pp)));
       }
-      rusanov_pp<KIND, DIM>(ql, plo, q, pm, a, A.pp, fl);
-      rusanov_pp<KIND, DIM>(q, pm, qh, phi, a, A.pp, fh);
-#pragma unroll
-      for (int k = 0; k < M; ++k) o[k] = __dsub_rn(o[k], __dmul_rn(coef[a], __dsub_rn(fh[k], fl[k])));
-    }
-    bool finite = true;
-#pragma unroll
-    for (int k = 0; k < M; ++k) {
-      A.out[((size_t)b * M + k) * NC + c] = o[k];
-      finite = finite && (fabs(o[k]) <= 1.7976931348623157e308);
-    }
-    if (A.status && !finite) atomicAdd(A.status + 1, 1u);
-    if (A.dt_slots) {
-      const auto pr = P::parts(o, A.pp);
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) atomicMax(sLam + a, maxkey(P::lam(o, pr, a, A.pp)));
     }
   }
   if (A.dt_slots) {

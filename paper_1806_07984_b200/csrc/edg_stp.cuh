@@ -1,11 +1,12 @@
 // Space-time predictor (Picard) kernel -- replaces kernels.py:120-159.
 //
 // Mapping: one thread per spatial node, CPB cells per
-// CTA.  A thread keeps the whole time column of its node in registers
+// CTA (~128-160 threads, so several CTAs -- and barrier domains -- share an
+// SM).  A thread keeps the whole time column of its node in registers
 // (qhat[n_t][m] and the next iterate acc[n_t][m]), so the K^-1 time
 // contraction is thread-local; the per-axis derivative contractions read the
 // flux of one time node from shared memory (double-buffered, one barrier per
-// time node), where all lanes of a pencil hit the same word (broadcast).
+// time node), where all lanes on one pencil read the same word (broadcast).
 //
 // Per Picard iteration and cell, with B[r][s] = K^-1[r][s] * (-dt w_s) and
 // c = K^-1 lift (kernels.py:134-142):
@@ -13,9 +14,10 @@
 // then delta = max |acc - qhat| over the cell (NaN-propagating, via 64-bit
 // atomicMax on bit patterns) decides the per-cell exit exactly like
 // kernels.py:143-147 (delta < tol).  Converged cells stop updating; the CTA
-// runs until its last cell stops.  The epilogue (kernels.py:148-157) forms
-// q_end, q_int and the time-integrated flux, stages them in shared memory and
-// projects them onto the 2d faces.
+// runs until its last cell stops (the solver orders cells by their previous
+// Picard count so that CTAs are homogeneous).  The epilogue
+// (kernels.py:148-157) forms q_end, q_int and the time-integrated flux,
+// stages them in shared memory and projects them onto the 2d faces.
 #pragma once
 #include "edg_common.cuh"
 
@@ -60,9 +62,11 @@ template <int DIM, int N>
 struct StpCfg {
   static constexpr int NPC = ipow(N, DIM);
   static constexpr int NF = ipow(N, DIM - 1);
-  static constexpr int TARGET = DIM == 2 ? 256 : 128;
+  static constexpr int TARGET = 128;
   static constexpr int CPB = stp_best_cpb(NPC, TARGET);
   static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32;
+  // resident CTAs per SM requested from ptxas (caps registers per thread)
+  static constexpr int MINB = THREADS <= 192 ? 3 : (THREADS <= 384 ? 1 : 1);
 };
 
 template <int KIND, int DIM, int N>
@@ -74,23 +78,8 @@ struct StpSmem {
   static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * FB) + sizeof(unsigned long long) * 2 * C::CPB;
 };
 
-// stride of axis a inside a cell's node block (last axis fastest)
-template <int DIM, int N>
-__device__ __forceinline__ constexpr int axis_stride(int a) {
-  return ipow(N, DIM - 1 - a);
-}
-
-// node index of face point f of face normal to axis a at normal index j
-template <int DIM, int N>
-__device__ __forceinline__ int face_node(int f, int a, int j) {
-  const int st = ipow(N, DIM - 1 - a);      // stride of axis a
-  const int hi = f / st;                    // axes before a
-  const int lo = f - hi * st;               // axes after a
-  return hi * st * N + j * st + lo;
-}
-
 template <int KIND, int DIM, int N>
-__global__ void __launch_bounds__(StpCfg<DIM, N>::THREADS)
+__global__ void __launch_bounds__(StpCfg<DIM, N>::THREADS, StpCfg<DIM, N>::MINB)
 stp_picard_kernel(const StpArgs A) {
   using P = Pde<KIND, DIM>;
   using Cf = StpCfg<DIM, N>;
@@ -116,7 +105,7 @@ stp_picard_kernel(const StpArgs A) {
   const int node = tid - slot * NPC;
   const int item = blockIdx.x * CPB + slot;
   const bool has_cell = (slot < CPB) && (item < A.nwork);
-  const int cell = has_cell ? (A.cell_list ? A.cell_list[item] : item) : 0;
+  const int cell = has_cell ? (A.cell_list ? __ldg(A.cell_list + item) : item) : 0;
   const double dt = *A.dt;
 
   for (int i = tid; i < N * N; i += THREADS) {
@@ -143,6 +132,10 @@ stp_picard_kernel(const StpArgs A) {
       t /= N;
     }
   }
+  // pencil base (node index with i_a = 0) per axis
+  int pb[DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) pb[a] = node - ix[a] * ipow(N, DIM - 1 - a);
   // derivative rows of this node, scaled by 1/h_a
   double Dr[DIM][N];
   {
@@ -155,45 +148,43 @@ stp_picard_kernel(const StpArgs A) {
     }
   }
 
-  double q0[M], qh[N][M], acc[N][M];
-  const size_t cbase = (size_t)cell * M * NPC;
+  const double* qsrc = A.q + (size_t)cell * M * NPC + node;
+  double qh[N][M], acc[N][M];
 #pragma unroll
-  for (int k = 0; k < M; ++k) q0[k] = has_cell ? A.q[cbase + (size_t)k * NPC + node] : 1.0;
+  for (int k = 0; k < M; ++k) {
+    const double v = has_cell ? __ldg(qsrc + k * NPC) : 1.0;
 #pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int k = 0; k < M; ++k) qh[r][k] = q0[k];
+    for (int r = 0; r < N; ++r) qh[r][k] = v;
+  }
 
   bool active = has_cell;
   int its = 0;
   bool conv = false;
   const int max_iter = A.max_iter;
+  double* myF = sF + slot * (DIM * M * NPC);
 
   for (int it = 1; it <= max_iter; ++it) {
     if (active) {
 #pragma unroll
-      for (int r = 0; r < N; ++r)
+      for (int k = 0; k < M; ++k) {
+        const double q0 = __ldg(qsrc + k * NPC);    // L1-resident initial state
 #pragma unroll
-        for (int k = 0; k < M; ++k) acc[r][k] = sC[r] * q0[k];
+        for (int r = 0; r < N; ++r) acc[r][k] = sC[r] * q0;
+      }
     }
 #pragma unroll
     for (int s = 0; s < N; ++s) {
-      double* Fb = sF + (s & 1) * Sm::FB + slot * (DIM * M * NPC);
+      double* Fb = myF + (s & 1) * Sm::FB;
       if (active) {
-        const auto pr = P::parts(qh[s], A.pp);
+        double F[DIM][M];
+        FastFlux<KIND, DIM>::template all<M>(qh[s], A.pp, F);
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-          double f[M];
-          P::flux(qh[s], pr, a, A.pp, f);
+        for (int a = 0; a < DIM; ++a)
 #pragma unroll
-          for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPC + node] = f[k];
-        }
+          for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPC + node] = F[a][k];
       }
       __syncthreads();
       if (active) {
-        double bcol[N];
-#pragma unroll
-        for (int r = 0; r < N; ++r) bcol[r] = sB[r * N + s];
 #pragma unroll
         for (int k = 0; k < M; ++k) {
           double dv = 0.0;
@@ -202,12 +193,12 @@ stp_picard_kernel(const StpArgs A) {
             constexpr int dummy = 0;
             (void)dummy;
             const int st = ipow(N, DIM - 1 - a);
-            const double* Fa = Fb + (a * M + k) * NPC + (node - ix[a] * st);
+            const double* Fa = Fb + (a * M + k) * NPC + pb[a];
 #pragma unroll
             for (int j = 0; j < N; ++j) dv = fma(Dr[a][j], Fa[j * st], dv);
           }
 #pragma unroll
-          for (int r = 0; r < N; ++r) acc[r][k] = fma(bcol[r], dv, acc[r][k]);
+          for (int r = 0; r < N; ++r) acc[r][k] = fma(sB[r * N + s], dv, acc[r][k]);
         }
       }
     }
@@ -240,12 +231,11 @@ stp_picard_kernel(const StpArgs A) {
   // ---------------------------------------------------------- epilogue --
   // q_end = sum_r l_r(1) qhat_r; q_int = dt sum_r w_r qhat_r;
   // fint_a = dt sum_r w_r F_a(qhat_r)          (kernels.py:148-155)
+  // staged as [slot][(1+DIM)*M][NPC] for the face projections
+  double* St = sF + slot * ((1 + DIM) * M * NPC);
   double qe[M], qi[M], fi[DIM][M];
 #pragma unroll
-  for (int k = 0; k < M; ++k) {
-    qe[k] = 0.0;
-    qi[k] = 0.0;
-  }
+  for (int k = 0; k < M; ++k) qe[k] = qi[k] = 0.0;
 #pragma unroll
   for (int a = 0; a < DIM; ++a)
 #pragma unroll
@@ -254,33 +244,65 @@ stp_picard_kernel(const StpArgs A) {
 #pragma unroll
     for (int r = 0; r < N; ++r) {
       const double tr = sTR[r], w = sW[r];
-      const auto pr = P::parts(qh[r], A.pp);
+      double F[DIM][M];
+      FastFlux<KIND, DIM>::template all<M>(qh[r], A.pp, F);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
         qe[k] = fma(tr, qh[r][k], qe[k]);
         qi[k] = fma(w, qh[r][k], qi[k]);
       }
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) {
-        double f[M];
-        P::flux(qh[r], pr, a, A.pp, f);
+      for (int a = 0; a < DIM; ++a)
 #pragma unroll
-        for (int k = 0; k < M; ++k) fi[a][k] = fma(w, f[k], fi[a][k]);
-      }
+        for (int k = 0; k < M; ++k) fi[a][k] = fma(w, F[a][k], fi[a][k]);
     }
+    double* qend = A.q_end + (size_t)cell * M * NPC + node;
+    double* qint = A.q_int ? A.q_int + (size_t)cell * M * NPC + node : nullptr;
 #pragma unroll
     for (int k = 0; k < M; ++k) {
       qi[k] *= dt;
-      A.q_end[cbase + (size_t)k * NPC + node] = qe[k];
-      if (A.q_int) A.q_int[cbase + (size_t)k * NPC + node] = qi[k];
+      qend[k * NPC] = qe[k];
+      if (qint) qint[k * NPC] = qi[k];
     }
-#pragma unroll
-    for (int a = 0; a < DIM; ++a)
-#pragma unroll
-      for (int k = 0; k < M; ++k) fi[a][k] *= dt;
     if (node == 0) {
       A.iterations[cell] = its;
       A.converged[cell] = conv ? 1 : 0;
+    }
+  }
+  // the flux buffers may still be read by other cells' last iteration until here
+  __syncthreads();
+  if (has_cell) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) St[k * NPC + node] = qi[k];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int k = 0; k < M; ++k) St[((1 + a) * M + k) * NPC + node] = fi[a][k] * dt;
+  }
+  __syncthreads();
+  if (has_cell) {
+    // outputs: family (trace_q from q_int, trace_f from fint_a) x face (a, s) x k x f
+    constexpr int PER_FAM = 2 * DIM * M * NF;
+    const size_t tbase = (size_t)cell * PER_FAM;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int st = ipow(N, DIM - 1 - a);
+      constexpr int ITEMS = 2 * 2 * M * NF;   // fam x s x k x f
+      for (int o = node; o < ITEMS; o += NPC) {
+        const int f = o % NF;
+        const int k = (o / NF) % M;
+        const int s = (o / (NF * M)) & 1;
+        const int fam = o / (2 * NF * M);
+        const int hi = f / st, lo = f - hi * st;
+        const double* src = St + ((fam == 0 ? 0 : (1 + a) * M) + k) * NPC + hi * st * N + lo;
+        const double* tv = s ? sTR : sTL;
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) v = fma(tv[j], src[j * st], v);
+        (fam == 0 ? A.trace_q : A.trace_f)[tbase + ((2 * a + s) * M + k) * NF + f] = v;
+      }
     }
   }
   if (A.iter_total) {
@@ -291,36 +313,6 @@ stp_picard_kernel(const StpArgs A) {
     if (has_cell && node == 0) atomicAdd(&sIts, (unsigned)its);
     __syncthreads();
     if (tid == 0 && sIts) atomicAdd(A.iter_total, (unsigned long long)sIts);
-  }
-  // stage q_int and fint for the face projections: [slot][(1+DIM)*M][NPC]
-  __syncthreads();
-  double* St = sF + slot * ((1 + DIM) * M * NPC);
-  if (has_cell) {
-#pragma unroll
-    for (int k = 0; k < M; ++k) St[k * NPC + node] = qi[k];
-#pragma unroll
-    for (int a = 0; a < DIM; ++a)
-#pragma unroll
-      for (int k = 0; k < M; ++k) St[((1 + a) * M + k) * NPC + node] = fi[a][k];
-  }
-  __syncthreads();
-  if (has_cell) {
-    constexpr int PER_FAM = 2 * DIM * M * NF;
-    const size_t tbase = (size_t)cell * PER_FAM;
-    for (int o = node; o < 2 * PER_FAM; o += NPC) {
-      const int fam = o / PER_FAM;
-      const int r = o - fam * PER_FAM;        // index inside [2d][M][NF]
-      const int fs = r / (M * NF);
-      const int k = (r / NF) % M;
-      const int f = r % NF;
-      const int a = fs >> 1, s = fs & 1;
-      const double* src = St + ((fam == 0 ? 0 : (1 + a) * M) + k) * NPC;
-      const double* tv = s ? sTR : sTL;
-      double v = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j) v = fma(tv[j], src[face_node<DIM, N>(f, a, j)], v);
-      (fam == 0 ? A.trace_q : A.trace_f)[tbase + r] = v;
-    }
   }
 }
 
