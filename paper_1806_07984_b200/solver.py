@@ -189,7 +189,7 @@ class DGSolver(_Base):
             self.hmin = torch.tensor([mesh.h], **f64)
             self.nbr = i32(mesh.nbr)
             # predictor work order: cells sorted by their last Picard count
-            self.order = torch.arange(Cn, dtype=torch.int32, device="cuda")
+            self.work_order = torch.arange(Cn, dtype=torch.int32, device="cuda")
             self.order_scratch = torch.zeros(128, dtype=torch.int32, device="cuda")
 
     # ---------------------------------------------------------------- state --
@@ -246,7 +246,7 @@ class DGSolver(_Base):
         if not self.adaptive:
             if tm:
                 tm.begin("stp")
-            _lib.check(self._stp(self.order, self.ncells), "stp_picard")
+            _lib.check(self._stp(self.work_order, self.ncells), "stp_picard")
             if tm:
                 tm.end("stp")
                 tm.begin("corrector")
@@ -257,7 +257,7 @@ class DGSolver(_Base):
                                          _lib.ptr(self.status), _stream()), "corrector")
             if tm:
                 tm.end("corrector")
-            _lib.check(lib.edg_order_by_iterations(self.ncells, _lib.ptr(self.iterations), _lib.ptr(self.order),
+            _lib.check(lib.edg_order_by_iterations(self.ncells, _lib.ptr(self.iterations), _lib.ptr(self.work_order),
                                                    _lib.ptr(self.order_scratch), _stream()), "order")
         else:
             nsk, F = self.nface_sk, self.mesh.nleaf
