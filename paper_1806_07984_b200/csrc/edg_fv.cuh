@@ -36,7 +36,9 @@ struct FvArgs {
 template <int DIM, int K>
 struct FvCfg {
   static constexpr int NC = ipow(K, DIM);
-  static constexpr int NE = ipow(K + 2, DIM);
+  static constexpr int KE = K + 2;                      // extended extent (face halos)
+  static constexpr int KEZ = (KE % 2) ? KE : KE + 1;    // last axis padded to an odd length
+  static constexpr int NE = ipow(KE, DIM - 1) * KEZ;    // (bank-conflict-free strided access)
   static constexpr int NL = ipow(K, DIM - 1);           // cells per layer / pencils per axis
   static constexpr int NI = (K + 1) * NL;               // interfaces per axis
   static constexpr int THREADS = NC >= 256 ? 256 : ((NC + 31) / 32) * 32;
@@ -56,7 +58,9 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
   using P = Pde<KIND, DIM>;
   using Cf = FvCfg<DIM, K>;
   constexpr int M = P::M;
-  constexpr int NC = Cf::NC, NE = Cf::NE, NL = Cf::NL, NI = Cf::NI, KE = K + 2;
+  constexpr int NC = Cf::NC, NE = Cf::NE, NL = Cf::NL, NI = Cf::NI, KE = Cf::KE, KEZ = Cf::KEZ;
+  // ext strides: last axis 1, then KEZ, then KEZ*KE
+  auto estride = [](int ax) { return ax == DIM - 1 ? 1 : (ax == DIM - 2 ? KEZ : KEZ * KE); };
   constexpr int THREADS = Cf::THREADS, CPT = Cf::CPT;
   constexpr bool EULER = KIND == EDG_PDE_EULER;
 
@@ -74,13 +78,12 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
   const double* src = A.patch + (size_t)b * M * NC;
 
   // ext index of a cell index (row-major, last axis fastest) shifted by +1
-  auto ext_of_cell = [](int c) {
-    int e = 0, mul = 1;
+  auto ext_of_cell = [&](int c) {
+    int e = 0;
 #pragma unroll
     for (int a = DIM - 1; a >= 0; --a) {
-      e += (c % K + 1) * mul;
+      e += (c % K + 1) * estride(a);
       c /= K;
-      mul *= KE;
     }
     return e;
   };
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
     }
     int x = 0;
 #pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) x = x * KE + (ax == a ? (s ? K + 1 : 0) : e[ax] + 1);
+    for (int ax = 0; ax < DIM; ++ax) x += (ax == a ? (s ? K + 1 : 0) : e[ax] + 1) * estride(ax);
     sQ[k * NE + x] = v;
   }
   __syncthreads();
@@ -140,10 +143,11 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
       // skip the unused edge / corner points of the extended block
       int t = i, outside = 0;
 #pragma unroll
-      for (int ax = 0; ax < DIM; ++ax) {
-        const int e = t % KE;
-        t /= KE;
-        outside += (e == 0 || e == K + 1);
+      for (int ax = DIM - 1; ax >= 0; --ax) {
+        const int ext = ax == DIM - 1 ? KEZ : KE;
+        const int e = t % ext;
+        t /= ext;
+        outside += (e == 0 || e == K + 1) + 2 * (e > K + 1);
       }
       if (outside > 1) continue;
       double q[M];
@@ -176,12 +180,12 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
     const double coef = __ddiv_rn(dt, __ddiv_rn(A.edges[a], (double)K));
     constexpr int dummy = 0;
     (void)dummy;
-    const int st = ipow(KE, DIM - 1 - a);
+    const int st = estride(a);
     // interfaces i = 0..K along a for every pencil p (the other axes)
     for (int it = tid; it < NI; it += THREADS) {
       const int i = it / NL, pcl = it - i * NL;
       // ext index of the state below the interface: index i along a, pencil +1 elsewhere
-      int t = pcl, x = 0, mul = 1;
+      int t = pcl, x = 0;
 #pragma unroll
       for (int ax = DIM - 1; ax >= 0; --ax) {
         int e;
@@ -191,8 +195,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
           e = t % K + 1;
           t /= K;
         }
-        x += e * mul;
-        mul *= KE;
+        x += e * estride(ax);
       }
       const int xl = x, xh = x + st;
       double ql[M], qh[M], f[M];
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
         rusanov<KIND, DIM>(ql, qh, a, 1, A.pp, f);
       }
 #pragma unroll
-      for (int k = 0; k < M; ++k) sFl[k * NI + it] = f[k];
+      for (int k = 0; k < M; ++k) sFl[k * NI + pcl * (K + 1) + i] = f[k];
     }
     __syncthreads();
 #pragma unroll
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
 #pragma unroll
         for (int k = 0; k < M; ++k)
           o[j][k] = __dsub_rn(o[j][k],
-                              __dmul_rn(coef, __dsub_rn(sFl[k * NI + (ia + 1) * NL + pcl], sFl[k * NI + ia * NL + pcl])));
+                              __dmul_rn(coef, __dsub_rn(sFl[k * NI + pcl * (K + 1) + ia + 1], sFl[k * NI + pcl * (K + 1) + ia])));
       }
     }
     __syncthreads();

@@ -78,8 +78,8 @@ struct StpSmem {
   static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * FB) + sizeof(unsigned long long) * 2 * C::CPB;
 };
 
-template <int KIND, int DIM, int N>
-__global__ void __launch_bounds__(StpCfg<DIM, N>::THREADS, StpCfg<DIM, N>::MINB)
+template <int KIND, int DIM, int N, int MINB = StpCfg<DIM, N>::MINB>
+__global__ void __launch_bounds__(StpCfg<DIM, N>::THREADS, MINB)
 stp_picard_kernel(const StpArgs A) {
   using P = Pde<KIND, DIM>;
   using Cf = StpCfg<DIM, N>;
@@ -89,6 +89,9 @@ stp_picard_kernel(const StpArgs A) {
   constexpr int NF = Cf::NF;
   constexpr int CPB = Cf::CPB;
   constexpr int THREADS = Cf::THREADS;
+  // flux buffer layout: node-major ([a][node][k], 16-byte accesses) for an
+  // even component count, component-major ([a][k][node]) otherwise
+  constexpr bool NODE_MAJOR = (M % 2 == 0);
 
   extern __shared__ __align__(16) double smem[];
   double* sD = smem;                 // D[N][N]
@@ -178,27 +181,56 @@ stp_picard_kernel(const StpArgs A) {
       if (active) {
         double F[DIM][M];
         FastFlux<KIND, DIM>::template all<M>(qh[s], A.pp, F);
+        if constexpr (NODE_MAJOR) {
+          // [a][node][k]: one node's components are contiguous -> 16-byte stores / loads
 #pragma unroll
-        for (int a = 0; a < DIM; ++a)
+          for (int a = 0; a < DIM; ++a)
 #pragma unroll
-          for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPC + node] = F[a][k];
+            for (int k2 = 0; k2 < M / 2; ++k2)
+              reinterpret_cast<double2*>(Fb + (a * NPC + node) * M)[k2] = make_double2(F[a][2 * k2], F[a][2 * k2 + 1]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < DIM; ++a)
+#pragma unroll
+            for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPC + node] = F[a][k];
+        }
       }
       __syncthreads();
       if (active) {
+        double dv[M];
 #pragma unroll
-        for (int k = 0; k < M; ++k) {
-          double dv = 0.0;
+        for (int k = 0; k < M; ++k) dv[k] = 0.0;
 #pragma unroll
-          for (int a = 0; a < DIM; ++a) {
-            constexpr int dummy = 0;
-            (void)dummy;
-            const int st = ipow(N, DIM - 1 - a);
-            const double* Fa = Fb + (a * M + k) * NPC + pb[a];
+        for (int a = 0; a < DIM; ++a) {
+          constexpr int dummy = 0;
+          (void)dummy;
+          const int st = ipow(N, DIM - 1 - a);
+          if constexpr (NODE_MAJOR) {
+            const double* Fa = Fb + (a * NPC + pb[a]) * M;
 #pragma unroll
-            for (int j = 0; j < N; ++j) dv = fma(Dr[a][j], Fa[j * st], dv);
+            for (int j = 0; j < N; ++j) {
+              const double2* p2 = reinterpret_cast<const double2*>(Fa + j * st * M);
+#pragma unroll
+              for (int k2 = 0; k2 < M / 2; ++k2) {
+                const double2 v = p2[k2];
+                dv[2 * k2] = fma(Dr[a][j], v.x, dv[2 * k2]);
+                dv[2 * k2 + 1] = fma(Dr[a][j], v.y, dv[2 * k2 + 1]);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+              const double* Fa = Fb + (a * M + k) * NPC + pb[a];
+#pragma unroll
+              for (int j = 0; j < N; ++j) dv[k] = fma(Dr[a][j], Fa[j * st], dv[k]);
+            }
           }
+        }
 #pragma unroll
-          for (int r = 0; r < N; ++r) acc[r][k] = fma(sB[r * N + s], dv, acc[r][k]);
+        for (int r = 0; r < N; ++r) {
+          const double b = sB[r * N + s];
+#pragma unroll
+          for (int k = 0; k < M; ++k) acc[r][k] = fma(b, dv[k], acc[r][k]);
         }
       }
     }

@@ -2,6 +2,8 @@
 // PDE-specialised kernel for the supported node counts and exposes host-side
 // launchers edg::unit_<name>_*.  Included by edg_k_*.cu with EDG_UNIT_KIND,
 // EDG_UNIT_DIM and EDG_UNIT_NAME defined (split for parallel nvcc builds).
+#include <cstdlib>
+
 #include "edg_stp.cuh"
 #include "edg_faces.cuh"
 #include "edg_fv.cuh"
@@ -33,7 +35,13 @@ static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
   using Cf = StpCfg<DIM, N>;
   const size_t smem = StpSmem<KIND, DIM, N>::BYTES;
-  auto kern = stp_picard_kernel<KIND, DIM, N>;
+  // EDG_STP_MINB=2 selects the 2-CTA/SM register budget (no spills) instead
+  // of the default 3-CTA/SM one (tuning knob, read once)
+  static const int minb = [] {
+    const char* v = getenv("EDG_STP_MINB");
+    return v ? atoi(v) : 0;
+  }();
+  auto kern = (minb == 2) ? stp_picard_kernel<KIND, DIM, N, 2> : stp_picard_kernel<KIND, DIM, N>;
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
   const int blocks = (a.nwork + Cf::CPB - 1) / Cf::CPB;
   if (blocks > 0) kern<<<blocks, Cf::THREADS, smem, st>>>(a);
