@@ -188,6 +188,22 @@ __device__ __forceinline__ double from_maxkey(unsigned long long k) {
 
 constexpr unsigned long long DT_EMPTY = 0xFFFFFFFFFFFFFFFFull;   // no candidate yet
 
+// Max of `key` over the lanes of this warp that share `seg` (segments are
+// contiguous lane ranges, e.g. the nodes of one cell), then one shared-memory
+// atomicMax per segment into base[seg].  All 32 lanes must call it; lanes
+// without data pass key = 0.
+__device__ __forceinline__ void seg_max_atomic(unsigned long long* base, int seg, unsigned long long key) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long v = __shfl_down_sync(0xffffffffu, key, off);
+    const int sv = __shfl_down_sync(0xffffffffu, seg, off);
+    if (lane + off < 32 && sv == seg && v > key) key = v;
+  }
+  const int prev = __shfl_up_sync(0xffffffffu, seg, 1);
+  if (seg >= 0 && key != 0ull && (lane == 0 || prev != seg)) atomicMax(base + seg, key);
+}
+
 // Python-max over axes of the per-axis node maxima (kernels.py:271-273):
 // lam = max(lam, ax) takes ax only if ax > lam, so a NaN axis is dropped.
 __device__ __forceinline__ double python_max(double lam, double ax) { return (ax > lam) ? ax : lam; }

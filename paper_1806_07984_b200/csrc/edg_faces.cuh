@@ -157,11 +157,15 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       A.q_out[cb + (size_t)k * NPC + node] = qn[k];
       finite = finite && (fabs(qn[k]) <= 1.7976931348623157e308);
     }
-    if (A.dt_slots) {
-      const auto pr = P::parts(qn, A.pp);
+  }
+  if (A.dt_slots) {
+    // per-cell per-axis max wave speed of the new state ([DIM][CPB] keys)
+    unsigned long long lk[DIM];
+    const auto pr = P::parts(qn, A.pp);
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) atomicMax(sLam + slot * DIM + a, maxkey(P::lam(qn, pr, a, A.pp)));
-    }
+    for (int a = 0; a < DIM; ++a) lk[a] = has_cell ? maxkey(P::lam(qn, pr, a, A.pp)) : 0ull;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) seg_max_atomic(sLam + a * CPB, has_cell ? slot : -1, lk[a]);
   }
   // per-cell non-finite flag (counted once per cell)
   if (has_cell && !finite) atomicOr(reinterpret_cast<unsigned int*>(sBest + slot), 1u);
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       if (c < A.ncells) {
         double lam = 0.0;
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) lam = python_max(lam, from_maxkey(sLam[tid * DIM + a]));
+        for (int a = 0; a < DIM; ++a) lam = python_max(lam, from_maxkey(sLam[a * CPB + tid]));
         if (lam > 0.0) {
           const double h = A.hmin[A.edges_per_cell ? c : 0];
           best = (unsigned long long)__double_as_longlong(dt_candidate(h, A.order, lam));

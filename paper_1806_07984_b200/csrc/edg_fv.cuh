@@ -260,11 +260,14 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
         finite = finite && (fabs(o[j][k]) <= 1.7976931348623157e308);
       }
       if (A.status && !finite) atomicAdd(A.status + 1, 1u);
-      if (A.dt_slots) {
-        const auto pr = P::parts(o[j], A.pp);
+    }
+    if (A.dt_slots) {
+      unsigned long long lk[DIM];
+      const auto pr = P::parts(o[j], A.pp);
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) atomicMax(sLam + a, maxkey(P::lam(o[j], pr, a, A.pp)));
-      }
+      for (int a = 0; a < DIM; ++a) lk[a] = c < NC ? maxkey(P::lam(o[j], pr, a, A.pp)) : 0ull;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) seg_max_atomic(sLam + a, 0, lk[a]);
     }
   }
   if (A.dt_slots) {

@@ -89,9 +89,10 @@ stp_picard_kernel(const StpArgs A) {
   constexpr int NF = Cf::NF;
   constexpr int CPB = Cf::CPB;
   constexpr int THREADS = Cf::THREADS;
-  // flux buffer layout: node-major ([a][node][k], 16-byte accesses) for an
-  // even component count, component-major ([a][k][node]) otherwise
-  constexpr bool NODE_MAJOR = (M % 2 == 0);
+  // flux buffer layout: component-major ([a][k][node]).  The node-major
+  // alternative ([a][node][k], 16-byte accesses) measured slower on cfg2
+  // (2-way bank conflicts from the 32-byte node stride), kept for reference.
+  constexpr bool NODE_MAJOR = false;
 
   extern __shared__ __align__(16) double smem[];
   double* sD = smem;                 // D[N][N]
@@ -235,8 +236,8 @@ stp_picard_kernel(const StpArgs A) {
       }
     }
     unsigned long long* red = sRed + (it & 1) * CPB;
+    unsigned long long mk = 0ull;
     if (active) {
-      unsigned long long mk = 0ull;
 #pragma unroll
       for (int r = 0; r < N; ++r)
 #pragma unroll
@@ -245,8 +246,8 @@ stp_picard_kernel(const StpArgs A) {
           mk = key > mk ? key : mk;
           qh[r][k] = acc[r][k];
         }
-      atomicMax(red + slot, mk);
     }
+    seg_max_atomic(red, slot < CPB ? slot : -1, mk);
     __syncthreads();
     if (active) {
       its = it;
