@@ -23,6 +23,20 @@ def stp_iter_flops(pde, d, n, m):
     return n ** (d + 1) * flux_flops(pde, d) + 2 * (d + 1) * m * n ** (d + 2) + (d + 2) * m * n ** (d + 1)
 
 
+def stp_iter1_flops(pde, d, n, m):
+    """First Picard iteration as the kernel executes it: qhat_s = q for every
+    time node, so one flux + one derivative per node and a rank-1 time
+    update (acc[r] = c_r q + (sum_s B[r][s]) div F(q))."""
+    return n ** d * flux_flops(pde, d) + 2 * d * m * n ** (d + 1) + 3 * m * n ** (d + 1)
+
+
+def stp_executed_flops(pde, d, n, m, cell_iterations, cell_steps):
+    """Flops the kernel executes for `cell_iterations` Picard iterations
+    summed over `cell_steps` cell-predictor evaluations."""
+    return (cell_steps * (stp_iter1_flops(pde, d, n, m) + stp_epilogue_flops(pde, d, n, m))
+            + (cell_iterations - cell_steps) * stp_iter_flops(pde, d, n, m))
+
+
 def stp_epilogue_flops(pde, d, n, m):
     return (4 * m * n ** (d + 1) + m * n ** d + 8 * d * m * n ** d + n ** (d + 1) * flux_flops(pde, d)
             + 2 * d * m * n ** (d + 1))

@@ -1,13 +1,16 @@
 // Patch finite-volume update -- replaces kernels.py:225-264.
 //
-// One CTA per k^d patch (256 threads; two CTAs resident per SM so one CTA's
-// loads overlap the other's arithmetic).  The patch and its 2d face halos (a
-// neighbour patch's boundary layer, kernels.py:256-264, or the own layer at
-// an outflow boundary) are staged once in shared memory as a (k+2)^d block,
-// together with the state-only parts of the flux (1/rho, p and the sound
-// speed for Euler), evaluated once per state.  Then, axis by axis in the
-// reference order a = 0..d-1, every unique interface flux of the patch is
-// evaluated once into a shared buffer and each volume applies
+// One CTA per k^d patch, one thread per volume (512 threads for 8^3; two
+// CTAs resident per SM so one CTA's loads overlap the other's arithmetic).
+// Each thread loads the m components of one state (its volume, then the 2d
+// face halos: a neighbour patch's boundary layer, kernels.py:256-264, or the
+// own layer at an outflow boundary), evaluates the state-only parts of the
+// flux once (1/rho, p and the sound speed for Euler) while the values are in
+// registers, and stages both in a (k+2)^d shared block whose last axis is
+// padded to an odd length (conflict-free strided access).  Then, axis by
+// axis in the reference order a = 0..d-1, every unique interface flux of the
+// patch is evaluated once into a pencil-major shared buffer and each volume
+// applies
 //     out -= (dt / dx_a) * (F_{i+1/2} - F_{i-1/2})
 // from the ORIGINAL states (unsplit, kernels.py:240-252).  Every operation is
 // the non-contracted round-to-nearest sequence of edg_common.cuh, so the
@@ -41,7 +44,7 @@ struct FvCfg {
   static constexpr int NE = ipow(KE, DIM - 1) * KEZ;    // (bank-conflict-free strided access)
   static constexpr int NL = ipow(K, DIM - 1);           // cells per layer / pencils per axis
   static constexpr int NI = (K + 1) * NL;               // interfaces per axis
-  static constexpr int THREADS = NC >= 256 ? 256 : ((NC + 31) / 32) * 32;
+  static constexpr int THREADS = NC >= 512 ? 512 : ((NC + 31) / 32) * 32;
   static constexpr int CPT = (NC + THREADS - 1) / THREADS;   // volumes per thread
 };
 
@@ -59,17 +62,17 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
   using Cf = FvCfg<DIM, K>;
   constexpr int M = P::M;
   constexpr int NC = Cf::NC, NE = Cf::NE, NL = Cf::NL, NI = Cf::NI, KE = Cf::KE, KEZ = Cf::KEZ;
-  // ext strides: last axis 1, then KEZ, then KEZ*KE
-  auto estride = [](int ax) { return ax == DIM - 1 ? 1 : (ax == DIM - 2 ? KEZ : KEZ * KE); };
   constexpr int THREADS = Cf::THREADS, CPT = Cf::CPT;
   constexpr bool EULER = KIND == EDG_PDE_EULER;
+  // ext strides: last axis 1, then KEZ, then KEZ*KE
+  auto estride = [](int ax) { return ax == DIM - 1 ? 1 : (ax == DIM - 2 ? KEZ : KEZ * KE); };
 
   extern __shared__ __align__(16) double smem[];
   double* sQ = smem;                               // [M][NE]
   double* sInv = sQ + M * NE;                      // [NE] (Euler)
   double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler)
   double* sC = sP + (EULER ? NE : 0);              // [NE] (Euler) sound speed
-  double* sFl = sC + (EULER ? NE : 0);             // [M][NI] interface fluxes of one axis
+  double* sFl = sC + (EULER ? NE : 0);             // [M][pencil][K+1] interface fluxes of one axis
   unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sFl + M * NI);
 
   const int b = blockIdx.x;
@@ -87,29 +90,34 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
     }
     return e;
   };
+  // stage one state (m components in registers) with its parts
+  auto stage = [&](int x, const double* q) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) sQ[k * NE + x] = q[k];
+    if constexpr (EULER) {
+      const auto pr = P::parts(q, A.pp);
+      sInv[x] = pr.inv;
+      sP[x] = pr.p;
+      sC[x] = __dsqrt_rn(__dmul_rn(__dmul_rn(A.pp.gamma, pr.p), pr.inv));
+    }
+  };
 
-  // ---- stage interior + halos (all loads issued before the stores) ----
-  {
-    constexpr int NLD = (M * NC + THREADS - 1) / THREADS;
-    double v[NLD];
+  // ---- interior states: thread = volume ----
+  double o[CPT][M];
+  int me[CPT];
 #pragma unroll
-    for (int i = 0; i < NLD; ++i) {
-      const int g = tid + i * THREADS;
-      v[i] = g < M * NC ? __ldg(src + g) : 0.0;
-    }
+  for (int j = 0; j < CPT; ++j) {
+    const int c = tid + j * THREADS;
+    me[j] = c < NC ? ext_of_cell(c) : 0;
 #pragma unroll
-    for (int i = 0; i < NLD; ++i) {
-      const int g = tid + i * THREADS;
-      if (g < M * NC) {
-        const int k = g / NC, c = g - k * NC;
-        sQ[k * NE + ext_of_cell(c)] = v[i];
-      }
-    }
+    for (int k = 0; k < M; ++k) o[j][k] = c < NC ? __ldg(src + k * NC + c) : 1.0;
   }
-  for (int i = tid; i < 2 * DIM * M * NL; i += THREADS) {
-    const int fs = i / (M * NL);
-    const int r = i - fs * M * NL;
-    const int k = r / NL, f = r - k * NL;
+#pragma unroll
+  for (int j = 0; j < CPT; ++j)
+    if (tid + j * THREADS < NC) stage(me[j], o[j]);
+  // ---- halo states: thread = one point of a face layer ----
+  for (int i = tid; i < 2 * DIM * NL; i += THREADS) {
+    const int fs = i / NL, f = i - fs * NL;
     const int a = fs >> 1, s = fs & 1;
     int e[DIM], t = f;
 #pragma unroll
@@ -118,9 +126,10 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
       e[ax] = t % K;
       t /= K;
     }
-    double v;
+    double q[M];
     if (A.halos) {
-      v = A.halos[(size_t)b * 2 * DIM * M * NL + i];
+#pragma unroll
+      for (int k = 0; k < M; ++k) q[k] = __ldg(A.halos + (((size_t)b * 2 * DIM + fs) * M + k) * NL + f);
     } else {
       const int nb = A.nbr[(size_t)b * 2 * DIM + fs];
       // neighbour below (s=0) contributes its last layer, above its first;
@@ -129,51 +138,17 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
       int c = 0;
 #pragma unroll
       for (int ax = 0; ax < DIM; ++ax) c = c * K + e[ax];
-      v = __ldg(A.patch + ((size_t)(nb >= 0 ? nb : b) * M + k) * NC + c);
+      const double* ps = A.patch + (size_t)(nb >= 0 ? nb : b) * M * NC + c;
+#pragma unroll
+      for (int k = 0; k < M; ++k) q[k] = __ldg(ps + k * NC);
     }
     int x = 0;
 #pragma unroll
     for (int ax = 0; ax < DIM; ++ax) x += (ax == a ? (s ? K + 1 : 0) : e[ax] + 1) * estride(ax);
-    sQ[k * NE + x] = v;
-  }
-  __syncthreads();
-  // ---- state parts once per staged state (Euler: 1/rho, p, c) ----
-  if constexpr (EULER) {
-    for (int i = tid; i < NE; i += THREADS) {
-      // skip the unused edge / corner points of the extended block
-      int t = i, outside = 0;
-#pragma unroll
-      for (int ax = DIM - 1; ax >= 0; --ax) {
-        const int ext = ax == DIM - 1 ? KEZ : KE;
-        const int e = t % ext;
-        t /= ext;
-        outside += (e == 0 || e == K + 1) + 2 * (e > K + 1);
-      }
-      if (outside > 1) continue;
-      double q[M];
-#pragma unroll
-      for (int k = 0; k < M; ++k) q[k] = sQ[k * NE + i];
-      const auto pr = P::parts(q, A.pp);
-      sInv[i] = pr.inv;
-      sP[i] = pr.p;
-      sC[i] = __dsqrt_rn(__dmul_rn(__dmul_rn(A.pp.gamma, pr.p), pr.inv));
-    }
+    stage(x, q);
   }
   const double dt = *A.dt;
-
-  // volumes owned by this thread, updated in registers across the axes
-  double o[CPT][M];
-  int me[CPT];
-#pragma unroll
-  for (int j = 0; j < CPT; ++j) {
-    const int c = tid + j * THREADS;
-    me[j] = c < NC ? ext_of_cell(c) : 0;
-  }
   __syncthreads();
-#pragma unroll
-  for (int j = 0; j < CPT; ++j)
-#pragma unroll
-    for (int k = 0; k < M; ++k) o[j][k] = sQ[k * NE + me[j]];
 
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
@@ -241,11 +216,11 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
         }
 #pragma unroll
         for (int k = 0; k < M; ++k)
-          o[j][k] = __dsub_rn(o[j][k],
-                              __dmul_rn(coef, __dsub_rn(sFl[k * NI + pcl * (K + 1) + ia + 1], sFl[k * NI + pcl * (K + 1) + ia])));
+          o[j][k] = __dsub_rn(o[j][k], __dmul_rn(coef, __dsub_rn(sFl[k * NI + pcl * (K + 1) + ia + 1],
+                                                                  sFl[k * NI + pcl * (K + 1) + ia])));
       }
     }
-    __syncthreads();
+    if (a + 1 < DIM) __syncthreads();
   }
 
   // ---- write back, non-finite count, next-step dt candidate ----

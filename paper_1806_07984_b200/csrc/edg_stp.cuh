@@ -66,14 +66,15 @@ struct StpCfg {
   static constexpr int CPB = stp_best_cpb(NPC, TARGET);
   static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32;
   // resident CTAs per SM requested from ptxas (caps registers per thread)
-  static constexpr int MINB = THREADS <= 192 ? 3 : (THREADS <= 384 ? 1 : 1);
+  // (measured: 2 for the 2-D p=5 kernel, 3 for the 3-D p=4 kernel)
+  static constexpr int MINB = DIM == 2 ? 2 : 3;
 };
 
 template <int KIND, int DIM, int N>
 struct StpSmem {
   using C = StpCfg<DIM, N>;
   static constexpr int M = Pde<KIND, DIM>::M;
-  static constexpr int OPS = 2 * N * N + 4 * N;                 // D, B, w, tr, tl, c
+  static constexpr int OPS = 2 * N * N + 6 * N;                 // D, B, w, tr, tl, c, Bsum (+pad)
   static constexpr int FB = C::CPB * DIM * M * C::NPC;          // one flux buffer
   static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * FB) + sizeof(unsigned long long) * 2 * C::CPB;
 };
@@ -89,10 +90,8 @@ stp_picard_kernel(const StpArgs A) {
   constexpr int NF = Cf::NF;
   constexpr int CPB = Cf::CPB;
   constexpr int THREADS = Cf::THREADS;
-  // flux buffer layout: component-major ([a][k][node]).  The node-major
-  // alternative ([a][node][k], 16-byte accesses) measured slower on cfg2
-  // (2-way bank conflicts from the 32-byte node stride), kept for reference.
-  constexpr bool NODE_MAJOR = false;
+  // flux buffer layout: component-major [a][k][node] (a node-major variant with
+  // 16-byte accesses measured slower: 2-way bank conflicts from the node stride)
 
   extern __shared__ __align__(16) double smem[];
   double* sD = smem;                 // D[N][N]
@@ -101,7 +100,8 @@ stp_picard_kernel(const StpArgs A) {
   double* sTL = sW + N;
   double* sTR = sTL + N;
   double* sC = sTR + N;              // K^-1 lift
-  double* sF = sC + N;               // flux buffers [2][CPB][DIM][M][NPC]
+  double* sBs = sC + N;              // sum_s B[r][s]
+  double* sF = sBs + N;              // flux buffers [2][CPB][DIM][M][NPC]
   unsigned long long* sRed = reinterpret_cast<unsigned long long*>(sF + 2 * Sm::FB);   // [2][CPB]
 
   const int tid = threadIdx.x;
@@ -123,6 +123,9 @@ stp_picard_kernel(const StpArgs A) {
     sTL[i] = A.basis[EDG_BASIS_TL(N) + i];
     sTR[i] = A.basis[EDG_BASIS_TR(N) + i];
     sC[i] = A.basis[EDG_BASIS_KLIFT(N) + i];
+    double bs = 0.0;
+    for (int s = 0; s < N; ++s) bs += A.basis[EDG_BASIS_KINV(N) + i * N + s] * (-dt * A.basis[EDG_BASIS_W(N) + s]);
+    sBs[i] = bs;
   }
   for (int i = tid; i < 2 * CPB; i += THREADS) sRed[i] = 0ull;
   __syncthreads();
@@ -165,74 +168,77 @@ stp_picard_kernel(const StpArgs A) {
   int its = 0;
   bool conv = false;
   const int max_iter = A.max_iter;
-  double* myF = sF + slot * (DIM * M * NPC);
+  double* const buf0 = sF + slot * (DIM * M * NPC);
+  double* const buf1 = buf0 + Sm::FB;
 
-  for (int it = 1; it <= max_iter; ++it) {
-    if (active) {
+  // flux of one time node of this node's column -> flux buffer [a][k][node]
+  auto put_flux = [&](double* Fb, const double* q) {
+    double F[DIM][M];
+    FastFlux<KIND, DIM>::template all<M>(q, A.pp, F);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPC + node] = F[a][k];
+  };
+  // dv[k] = sum_a sum_j (D/h_a)[i_a][j] F_a[k][pencil_a(j)]
+  auto deriv = [&](const double* Fb, double (&dv)[M]) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) dv[k] = 0.0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const int st = ipow(N, DIM - 1 - a);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        const double q0 = __ldg(qsrc + k * NPC);    // L1-resident initial state
+        const double* Fa = Fb + (a * M + k) * NPC + pb[a];
 #pragma unroll
-        for (int r = 0; r < N; ++r) acc[r][k] = sC[r] * q0;
+        for (int j = 0; j < N; ++j) dv[k] = fma(Dr[a][j], Fa[j * st], dv[k]);
       }
     }
-#pragma unroll
-    for (int s = 0; s < N; ++s) {
-      double* Fb = myF + (s & 1) * Sm::FB;
-      if (active) {
-        double F[DIM][M];
-        FastFlux<KIND, DIM>::template all<M>(qh[s], A.pp, F);
-        if constexpr (NODE_MAJOR) {
-          // [a][node][k]: one node's components are contiguous -> 16-byte stores / loads
-#pragma unroll
-          for (int a = 0; a < DIM; ++a)
-#pragma unroll
-            for (int k2 = 0; k2 < M / 2; ++k2)
-              reinterpret_cast<double2*>(Fb + (a * NPC + node) * M)[k2] = make_double2(F[a][2 * k2], F[a][2 * k2 + 1]);
-        } else {
-#pragma unroll
-          for (int a = 0; a < DIM; ++a)
-#pragma unroll
-            for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPC + node] = F[a][k];
-        }
-      }
+  };
+
+  for (int it = 1; it <= max_iter; ++it) {
+    if (it == 1) {
+      // qhat_s = q for every time node (kernels.py:134), so the first
+      // iteration needs one flux and one derivative:
+      //   acc[r] = c_r q + (sum_s B[r][s]) div F(q)
+      if (active) put_flux(buf0, qh[0]);
       __syncthreads();
       if (active) {
         double dv[M];
+        deriv(buf0, dv);
 #pragma unroll
-        for (int k = 0; k < M; ++k) dv[k] = 0.0;
+        for (int k = 0; k < M; ++k) {
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-          constexpr int dummy = 0;
-          (void)dummy;
-          const int st = ipow(N, DIM - 1 - a);
-          if constexpr (NODE_MAJOR) {
-            const double* Fa = Fb + (a * NPC + pb[a]) * M;
+          for (int r = 0; r < N; ++r) acc[r][k] = fma(sBs[r], dv[k], sC[r] * qh[r][k]);
+        }
+      }
+    } else {
+      if (active) {
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-              const double2* p2 = reinterpret_cast<const double2*>(Fa + j * st * M);
+        for (int k = 0; k < M; ++k) {
+          const double q0 = __ldg(qsrc + k * NPC);    // L1-resident initial state
 #pragma unroll
-              for (int k2 = 0; k2 < M / 2; ++k2) {
-                const double2 v = p2[k2];
-                dv[2 * k2] = fma(Dr[a][j], v.x, dv[2 * k2]);
-                dv[2 * k2 + 1] = fma(Dr[a][j], v.y, dv[2 * k2 + 1]);
-              }
-            }
-          } else {
+          for (int r = 0; r < N; ++r) acc[r][k] = sC[r] * q0;
+        }
+        put_flux(buf0, qh[0]);
+      }
+      __syncthreads();
+      // software pipeline: the flux of time node s+1 is evaluated and stored
+      // (other buffer) while the derivative of time node s is contracted
 #pragma unroll
-            for (int k = 0; k < M; ++k) {
-              const double* Fa = Fb + (a * M + k) * NPC + pb[a];
+      for (int s = 0; s < N; ++s) {
+        if (active) {
+          if (s + 1 < N) put_flux(((s + 1) & 1) ? buf1 : buf0, qh[s + 1]);
+          double dv[M];
+          deriv((s & 1) ? buf1 : buf0, dv);
 #pragma unroll
-              for (int j = 0; j < N; ++j) dv[k] = fma(Dr[a][j], Fa[j * st], dv[k]);
-            }
+          for (int r = 0; r < N; ++r) {
+            const double b = sB[r * N + s];
+#pragma unroll
+            for (int k = 0; k < M; ++k) acc[r][k] = fma(b, dv[k], acc[r][k]);
           }
         }
-#pragma unroll
-        for (int r = 0; r < N; ++r) {
-          const double b = sB[r * N + s];
-#pragma unroll
-          for (int k = 0; k < M; ++k) acc[r][k] = fma(b, dv[k], acc[r][k]);
-        }
+        __syncthreads();
       }
     }
     unsigned long long* red = sRed + (it & 1) * CPB;
