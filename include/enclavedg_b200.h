@@ -179,6 +179,9 @@ int edg_patch_boundary_layers(int32_t dim, int32_t m, int32_t k, int32_t npatche
  * on `stream`; used by bench.py for the FP64 roofline denominator, which
  * MEASURED_PEAKS.json does not carry. */
 int edg_probe_fp64(double* sink_dev, int32_t blocks, int32_t iters, void* stream);
+/* DMMA (mma.sync m8n8k4 f64) probe: blocks x 8 warps x 4 chains x iters
+ * MMAs of 8*8*4 FMAs each (flops = blocks * 8 * 4 * iters * 512). */
+int edg_probe_dmma(double* sink_dev, int32_t blocks, int32_t iters, void* stream);
 
 /* ---- stream schedule helpers --------------------------------------------- */
 /* Priority range of the device (numerically lower = higher priority). */

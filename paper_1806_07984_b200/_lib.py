@@ -37,6 +37,7 @@ SIGNATURES = {
     "edg_last_error": (C.c_char_p, []),
     "edg_stp_picard": (C.c_int, [PDEP, I32, P, P, P, I32, P, I32, P, D, I32, P, P, P, P, P, P, P, P]),
     "edg_probe_fp64": (C.c_int, [P, I32, I32, P]),
+    "edg_probe_dmma": (C.c_int, [P, I32, I32, P]),
     "edg_order_by_iterations": (C.c_int, [I32, P, P, P, P]),
     "edg_project_to_faces": (C.c_int, [I32, I32, I32, P, I32, P, P, P]),
     "edg_riemann_rusanov": (C.c_int, [PDEP, I32, I32, P, P, I32, I32, P, P]),

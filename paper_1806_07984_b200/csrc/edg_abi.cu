@@ -370,7 +370,31 @@ static __global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, in
   if (s == 123.456) sink[0] = s;   // never true; keeps the chains alive
 }
 
+// DMMA (mma.sync m8n8k4 f64) throughput probe: 4 independent accumulators per warp
+static __global__ void __launch_bounds__(256) dmma_probe_kernel(double* sink, int iters) {
+  double a = 1.0 + 1e-9 * threadIdx.x, b = 0.5 - 1e-9 * threadIdx.x;
+  double c[4][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) c[u][0] = c[u][1] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                   : "+d"(c[u][0]), "+d"(c[u][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) s += c[u][0] + c[u][1];
+  if (s == 123.456) sink[0] = s;
+}
+
 extern "C" {
+
+int edg_probe_dmma(double* sink_dev, int32_t blocks, int32_t iters, void* stream) {
+  dmma_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink_dev, iters);
+  return cuda_status(check_launch());
+}
 
 int edg_order_by_iterations(int32_t ncells, const int32_t* iterations_dev, int32_t* order_dev,
                             int32_t* scratch_dev, void* stream) {
