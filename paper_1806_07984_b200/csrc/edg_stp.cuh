@@ -75,7 +75,11 @@ struct StpSmem {
   using C = StpCfg<DIM, N>;
   static constexpr int M = Pde<KIND, DIM>::M;
   static constexpr int OPS = 2 * N * N + 6 * N;                 // D, B, w, tr, tl, c, Bsum (+pad)
-  static constexpr int FB = C::CPB * DIM * M * C::NPC;          // one flux buffer
+  // flux buffers pad the last (contiguous) axis to an even length NP so that
+  // pencil pairs along it are 16-byte aligned
+  static constexpr int NP = N + (N & 1);
+  static constexpr int NPCP = C::NPC / N * NP;
+  static constexpr int FB = C::CPB * DIM * M * NPCP;            // one flux buffer
   static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * FB) + sizeof(unsigned long long) * 2 * C::CPB;
 };
 
@@ -140,9 +144,11 @@ stp_picard_kernel(const StpArgs A) {
     }
   }
   // pencil base (node index with i_a = 0) per axis
+  constexpr int NP = Sm::NP, NPCP = Sm::NPCP;
+  const int bnode = (node / N) * NP + node % N;   // node index in the padded flux buffer
   int pb[DIM];
 #pragma unroll
-  for (int a = 0; a < DIM; ++a) pb[a] = node - ix[a] * ipow(N, DIM - 1 - a);
+  for (int a = 0; a < DIM; ++a) pb[a] = bnode - ix[a] * (a == DIM - 1 ? 1 : NP * ipow(N, DIM - 2 - a));
   // derivative rows of this node, scaled by 1/h_a
   double Dr[DIM][N];
   {
@@ -168,7 +174,7 @@ stp_picard_kernel(const StpArgs A) {
   int its = 0;
   bool conv = false;
   const int max_iter = A.max_iter;
-  double* const buf0 = sF + slot * (DIM * M * NPC);
+  double* const buf0 = sF + slot * (DIM * M * NPCP);
   double* const buf1 = buf0 + Sm::FB;
 
   // flux of one time node of this node's column -> flux buffer [a][k][node]
@@ -178,21 +184,41 @@ stp_picard_kernel(const StpArgs A) {
 #pragma unroll
     for (int a = 0; a < DIM; ++a)
 #pragma unroll
-      for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPC + node] = F[a][k];
+      for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPCP + bnode] = F[a][k];
   };
   // dv[k] = sum_a sum_j (D/h_a)[i_a][j] F_a[k][pencil_a(j)]
   auto deriv = [&](const double* Fb, double (&dv)[M]) {
-#pragma unroll
-    for (int k = 0; k < M; ++k) dv[k] = 0.0;
+    // one independent FMA chain per (axis, component) for ILP; summed at the end
+    double part[DIM][M];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-      const int st = ipow(N, DIM - 1 - a);
+      const int st = a == DIM - 1 ? 1 : NP * ipow(N, DIM - 2 - a);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        const double* Fa = Fb + (a * M + k) * NPC + pb[a];
+        const double* Fa = Fb + (a * M + k) * NPCP + pb[a];
+        double acc_ak = 0.0;
+        if (a == DIM - 1) {
+          // contiguous pencil: 16-byte pair loads (lanes of one pencil broadcast)
 #pragma unroll
-        for (int j = 0; j < N; ++j) dv[k] = fma(Dr[a][j], Fa[j * st], dv[k]);
+          for (int j = 0; j + 1 < N; j += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(Fa + j);
+            acc_ak = fma(Dr[a][j], v.x, acc_ak);
+            acc_ak = fma(Dr[a][j + 1], v.y, acc_ak);
+          }
+          if (N & 1) acc_ak = fma(Dr[a][N - 1], Fa[N - 1], acc_ak);
+        } else {
+#pragma unroll
+          for (int j = 0; j < N; ++j) acc_ak = fma(Dr[a][j], Fa[j * st], acc_ak);
+        }
+        part[a][k] = acc_ak;
       }
+    }
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      double v = part[0][k];
+#pragma unroll
+      for (int a = 1; a < DIM; ++a) v += part[a][k];
+      dv[k] = v;
     }
   };
 
