@@ -105,7 +105,8 @@ stp_picard_kernel(const StpArgs A) {
   double* sTR = sTL + N;
   double* sC = sTR + N;              // K^-1 lift
   double* sBs = sC + N;              // sum_s B[r][s]
-  double* sF = sBs + N;              // flux buffers [2][CPB][DIM][M][NPC]
+  double* sF = smem + Sm::OPS;       // flux buffers [2][CPB][DIM][M][NPCP], 16-byte aligned (OPS even)
+  static_assert(Sm::OPS % 2 == 0 && Sm::OPS >= 2 * N * N + 5 * N, "operator block must keep sF 16-byte aligned");
   unsigned long long* sRed = reinterpret_cast<unsigned long long*>(sF + 2 * Sm::FB);   // [2][CPB]
 
   const int tid = threadIdx.x;
