@@ -77,7 +77,7 @@ struct StpSmem {
   static constexpr int OPS = 2 * N * N + 6 * N;                 // D, B, w, tr, tl, c, Bsum (+pad)
   // flux buffers pad the last (contiguous) axis to an even length NP so that
   // pencil pairs along it are 16-byte aligned
-  static constexpr int NP = N + (N & 1);
+  static constexpr int NP = N;   // (padding odd N to N+1 for pair loads measured slower on 3-D p=4)
   static constexpr int NPCP = C::NPC / N * NP;
   static constexpr int FB = C::CPB * DIM * M * NPCP;            // one flux buffer
   static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * FB) + sizeof(unsigned long long) * 2 * C::CPB;
@@ -198,7 +198,7 @@ stp_picard_kernel(const StpArgs A) {
       for (int k = 0; k < M; ++k) {
         const double* Fa = Fb + (a * M + k) * NPCP + pb[a];
         double acc_ak = 0.0;
-        if (a == DIM - 1) {
+        if (a == DIM - 1 && (N % 2 == 0)) {
           // contiguous pencil: 16-byte pair loads (lanes of one pencil broadcast)
 #pragma unroll
           for (int j = 0; j + 1 < N; j += 2) {

@@ -66,6 +66,7 @@ class _Base:
         self.max_steps = max_steps
         self._graph = None
         self._graph_steps = 0
+        self._graph_key = None
         self.kernel_timer = None      # optional KernelTimer (events around the hot kernels)
 
     def _finalize_dt(self):
@@ -104,24 +105,32 @@ class _Base:
         if full and self.steps_done + full * chunk > self.max_steps:
             raise ConfigError("dt history too short: raise max_steps")
         if full:
-            if self._graph is None or self._graph_steps != chunk:
-                # capture from a step whose parity matches replay
-                side = torch.cuda.Stream()
-                side.wait_stream(torch.cuda.current_stream())
-                g = torch.cuda.CUDAGraph()
-                base = self.steps_done
-                with torch.cuda.stream(side):
-                    with torch.cuda.graph(g, stream=side):
-                        for k in range(chunk):
-                            self._enqueue_step()
-                torch.cuda.current_stream().wait_stream(side)
-                self._graph, self._graph_steps = g, chunk
-                self.steps_done = base          # capture does not execute
+            self.prepare_graph(chunk)
             for _ in range(full):
                 self._graph.replay()
                 self.steps_done += chunk
         for _ in range(steps - full * chunk):
             self.step()
+
+    def prepare_graph(self, chunk: int = 2):
+        """Capture `chunk` steps into a CUDA graph (once).  The graph bakes in
+        which physical buffer holds the state, so it is re-captured when an
+        odd number of eager steps has swapped the ping-pong roles."""
+        torch = self.torch
+        if chunk % 2:
+            raise ConfigError("graph chunk must be even (ping-pong buffers)")
+        key = (chunk, self.Q.data_ptr())
+        if self._graph is not None and self._graph_key == key:
+            return
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(chunk):
+                    self._enqueue_step()
+        torch.cuda.current_stream().wait_stream(side)
+        self._graph, self._graph_steps, self._graph_key = g, chunk, key
 
     def step(self):
         self._enqueue_step()
