@@ -1,16 +1,18 @@
 // Patch finite-volume update -- replaces kernels.py:225-264.
 //
-// One CTA per k^d patch, one thread per volume (512 threads for 8^3; two
-// CTAs resident per SM so one CTA's loads overlap the other's arithmetic).
-// Each thread loads the m components of one state (its volume, then the 2d
-// face halos: a neighbour patch's boundary layer, kernels.py:256-264, or the
-// own layer at an outflow boundary), evaluates the state-only parts of the
-// flux once (1/rho, p and the sound speed for Euler) while the values are in
+// One CTA per k^d patch (256 threads for 8^3, two volumes per thread along
+// the contiguous axis; three CTAs resident per SM).  Each thread loads the m
+// components of a state (the patch volumes, then the 2d face halos: a
+// neighbour patch's boundary layer, kernels.py:256-264, or the own layer at
+// an outflow boundary), evaluates the state-only parts of the flux once
+// (1/rho, p and the sound speed for Euler) while the values are in
 // registers, and stages both in a (k+2)^d shared block whose last axis is
-// padded to an odd length (conflict-free strided access).  Then, axis by
-// axis in the reference order a = 0..d-1, every unique interface flux of the
-// patch is evaluated once into a pencil-major shared buffer and each volume
-// applies
+// padded to an odd length (conflict-free strided access).  After a single
+// barrier every thread evaluates the interface fluxes of its volumes itself
+// -- both neighbours of an interface evaluate it with identical inputs in the
+// same (lo, hi) order, hence identically, and the interface between a
+// thread's own two volumes is evaluated once -- and applies, in the
+// reference order a = 0..d-1,
 //     out -= (dt / dx_a) * (F_{i+1/2} - F_{i-1/2})
 // from the ORIGINAL states (unsplit, kernels.py:240-252).  Every operation is
 // the non-contracted round-to-nearest sequence of edg_common.cuh, so the
@@ -42,26 +44,25 @@ struct FvCfg {
   static constexpr int KE = K + 2;                      // extended extent (face halos)
   static constexpr int KEZ = (KE % 2) ? KE : KE + 1;    // last axis padded to an odd length
   static constexpr int NE = ipow(KE, DIM - 1) * KEZ;    // (bank-conflict-free strided access)
-  static constexpr int NL = ipow(K, DIM - 1);           // cells per layer / pencils per axis
-  static constexpr int NI = (K + 1) * NL;               // interfaces per axis
-  static constexpr int THREADS = NC >= 512 ? 512 : ((NC + 31) / 32) * 32;
-  static constexpr int CPT = (NC + THREADS - 1) / THREADS;   // volumes per thread
+  static constexpr int NL = ipow(K, DIM - 1);           // cells per face layer
+  static constexpr int CPT = (K % 2 == 0 && NC >= 256) ? 2 : 1;   // volumes per thread (pairs along the last axis)
+  static constexpr int THREADS = ((NC / CPT + 31) / 32) * 32;
+  static constexpr int MINB = THREADS <= 256 ? 3 : 1;
 };
 
 template <int KIND, int DIM, int K>
 struct FvSmem {
   static constexpr int M = Pde<KIND, DIM>::M;
   static constexpr int NPARTS = KIND == EDG_PDE_EULER ? 3 : 0;
-  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + FvCfg<DIM, K>::NI * M) +
-                                  sizeof(unsigned long long) * DIM;
+  static constexpr size_t BYTES = sizeof(double) * FvCfg<DIM, K>::NE * (M + NPARTS) + sizeof(unsigned long long) * DIM;
 };
 
-template <int KIND, int DIM, int K>
-__global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(const FvArgs A) {
+template <int KIND, int DIM, int K, int MINB = FvCfg<DIM, K>::MINB>
+__global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(const FvArgs A) {
   using P = Pde<KIND, DIM>;
   using Cf = FvCfg<DIM, K>;
   constexpr int M = P::M;
-  constexpr int NC = Cf::NC, NE = Cf::NE, NL = Cf::NL, NI = Cf::NI, KE = Cf::KE, KEZ = Cf::KEZ;
+  constexpr int NC = Cf::NC, NE = Cf::NE, NL = Cf::NL, KE = Cf::KE, KEZ = Cf::KEZ;
   constexpr int THREADS = Cf::THREADS, CPT = Cf::CPT;
   constexpr bool EULER = KIND == EDG_PDE_EULER;
   // ext strides: last axis 1, then KEZ, then KEZ*KE
@@ -72,8 +73,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
   double* sInv = sQ + M * NE;                      // [NE] (Euler)
   double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler)
   double* sC = sP + (EULER ? NE : 0);              // [NE] (Euler) sound speed
-  double* sFl = sC + (EULER ? NE : 0);             // [M][pencil][K+1] interface fluxes of one axis
-  unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sFl + M * NI);
+  unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sC + (EULER ? NE : 0));
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
@@ -90,6 +90,11 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
     }
     return e;
   };
+  struct State {
+    double q[M];
+    typename P::Parts pr;
+    double c;
+  };
   // stage one state (m components in registers) with its parts
   auto stage = [&](int x, const double* q) {
 #pragma unroll
@@ -101,20 +106,38 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
       sC[x] = __dsqrt_rn(__dmul_rn(__dmul_rn(A.pp.gamma, pr.p), pr.inv));
     }
   };
+  auto load = [&](int x, State& s) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) s.q[k] = sQ[k * NE + x];
+    if constexpr (EULER) {
+      s.pr = {sInv[x], sP[x]};
+      s.c = sC[x];
+    }
+  };
+  // Rusanov flux along +a between lo and hi (kernels.py:162-173), exact order
+  auto iface = [&](const State& lo, const State& hi, int a, double* f) {
+    if constexpr (EULER) {
+      const double ul = __dmul_rn(P::mom(lo.q, a), lo.pr.inv), uh = __dmul_rn(P::mom(hi.q, a), hi.pr.inv);
+      const double lam = nan_max(__dadd_rn(fabs(ul), lo.c), __dadd_rn(fabs(uh), hi.c));
+      double fl[M], fh[M];
+      P::flux(lo.q, lo.pr, a, A.pp, fl);
+      P::flux(hi.q, hi.pr, a, A.pp, fh);
+      const double hl = __dmul_rn(0.5, lam);
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        f[k] = __dsub_rn(__dmul_rn(0.5, __dadd_rn(fl[k], fh[k])), __dmul_rn(hl, __dsub_rn(hi.q[k], lo.q[k])));
+    } else {
+      rusanov<KIND, DIM>(lo.q, hi.q, a, 1, A.pp, f);
+    }
+  };
 
   // ---- interior states: thread = volume ----
-  double o[CPT][M];
-  int me[CPT];
+  for (int c = tid; c < NC; c += THREADS) {
+    double q[M];
 #pragma unroll
-  for (int j = 0; j < CPT; ++j) {
-    const int c = tid + j * THREADS;
-    me[j] = c < NC ? ext_of_cell(c) : 0;
-#pragma unroll
-    for (int k = 0; k < M; ++k) o[j][k] = c < NC ? __ldg(src + k * NC + c) : 1.0;
+    for (int k = 0; k < M; ++k) q[k] = __ldg(src + k * NC + c);
+    stage(ext_of_cell(c), q);
   }
-#pragma unroll
-  for (int j = 0; j < CPT; ++j)
-    if (tid + j * THREADS < NC) stage(me[j], o[j]);
   // ---- halo states: thread = one point of a face layer ----
   for (int i = tid; i < 2 * DIM * NL; i += THREADS) {
     const int fs = i / NL, f = i - fs * NL;
@@ -150,84 +173,56 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
   const double dt = *A.dt;
   __syncthreads();
 
+  // ---- own volumes (CPT consecutive along the last axis) ----
+  const int c0 = tid * CPT;
+  const bool ok = c0 < NC;
+  const int x0 = ok ? ext_of_cell(c0) : ext_of_cell(0);
+  State me[CPT];
+  double o[CPT][M];
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    load(x0 + j, me[j]);
+#pragma unroll
+    for (int k = 0; k < M; ++k) o[j][k] = me[j].q[k];
+  }
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
     const double coef = __ddiv_rn(dt, __ddiv_rn(A.edges[a], (double)K));
-    constexpr int dummy = 0;
-    (void)dummy;
     const int st = estride(a);
-    // interfaces i = 0..K along a for every pencil p (the other axes)
-    for (int it = tid; it < NI; it += THREADS) {
-      const int i = it / NL, pcl = it - i * NL;
-      // ext index of the state below the interface: index i along a, pencil +1 elsewhere
-      int t = pcl, x = 0;
-#pragma unroll
-      for (int ax = DIM - 1; ax >= 0; --ax) {
-        int e;
-        if (ax == a) {
-          e = i;
-        } else {
-          e = t % K + 1;
-          t /= K;
-        }
-        x += e * estride(ax);
-      }
-      const int xl = x, xh = x + st;
-      double ql[M], qh[M], f[M];
+    if (a == DIM - 1 && CPT == 2) {
+      // interfaces (x0-1 | x0), (x0 | x0+1) shared, (x0+1 | x0+2)
+      State nb;
+      double fL[M], fM[M], fU[M];
+      load(x0 - 1, nb);
+      iface(nb, me[0], a, fL);
+      iface(me[0], me[1], a, fM);
+      load(x0 + 2, nb);
+      iface(me[1], nb, a, fU);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        ql[k] = sQ[k * NE + xl];
-        qh[k] = sQ[k * NE + xh];
+        o[0][k] = __dsub_rn(o[0][k], __dmul_rn(coef, __dsub_rn(fM[k], fL[k])));
+        o[1][k] = __dsub_rn(o[1][k], __dmul_rn(coef, __dsub_rn(fU[k], fM[k])));
       }
-      if constexpr (EULER) {
-        const typename P::Parts pl{sInv[xl], sP[xl]}, ph{sInv[xh], sP[xh]};
-        const double ul = __dmul_rn(ql[1 + a], pl.inv), uh = __dmul_rn(qh[1 + a], ph.inv);
-        const double lam = nan_max(__dadd_rn(fabs(ul), sC[xl]), __dadd_rn(fabs(uh), sC[xh]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        State nb;
         double fl[M], fh[M];
-        P::flux(ql, pl, a, A.pp, fl);
-        P::flux(qh, ph, a, A.pp, fh);
-        const double hl = __dmul_rn(0.5, lam);
+        load(x0 + j - st, nb);
+        iface(nb, me[j], a, fl);
+        load(x0 + j + st, nb);
+        iface(me[j], nb, a, fh);
 #pragma unroll
-        for (int k = 0; k < M; ++k)
-          f[k] = __dsub_rn(__dmul_rn(0.5, __dadd_rn(fl[k], fh[k])), __dmul_rn(hl, __dsub_rn(qh[k], ql[k])));
-      } else {
-        rusanov<KIND, DIM>(ql, qh, a, 1, A.pp, f);
-      }
-#pragma unroll
-      for (int k = 0; k < M; ++k) sFl[k * NI + pcl * (K + 1) + i] = f[k];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < CPT; ++j) {
-      const int c = tid + j * THREADS;
-      if (c < NC) {
-        // cell index along a and its pencil (the other axes in order)
-        int t = c, ia = 0, pcl = 0, mul = 1;
-#pragma unroll
-        for (int ax = DIM - 1; ax >= 0; --ax) {
-          const int e = t % K;
-          t /= K;
-          if (ax == a) {
-            ia = e;
-          } else {
-            pcl += e * mul;
-            mul *= K;
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < M; ++k)
-          o[j][k] = __dsub_rn(o[j][k], __dmul_rn(coef, __dsub_rn(sFl[k * NI + pcl * (K + 1) + ia + 1],
-                                                                  sFl[k * NI + pcl * (K + 1) + ia])));
+        for (int k = 0; k < M; ++k) o[j][k] = __dsub_rn(o[j][k], __dmul_rn(coef, __dsub_rn(fh[k], fl[k])));
       }
     }
-    if (a + 1 < DIM) __syncthreads();
   }
 
   // ---- write back, non-finite count, next-step dt candidate ----
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
-    const int c = tid + j * THREADS;
-    if (c < NC) {
+    const int c = c0 + j;
+    if (ok) {
       bool finite = true;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
@@ -240,7 +235,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_patch_kernel(con
       unsigned long long lk[DIM];
       const auto pr = P::parts(o[j], A.pp);
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) lk[a] = c < NC ? maxkey(P::lam(o[j], pr, a, A.pp)) : 0ull;
+      for (int a = 0; a < DIM; ++a) lk[a] = ok ? maxkey(P::lam(o[j], pr, a, A.pp)) : 0ull;
 #pragma unroll
       for (int a = 0; a < DIM; ++a) seg_max_atomic(sLam + a, 0, lk[a]);
     }

@@ -189,7 +189,9 @@ stp_picard_kernel(const StpArgs A) {
   };
   // dv[k] = sum_a sum_j (D/h_a)[i_a][j] F_a[k][pencil_a(j)]
   auto deriv = [&](const double* Fb, double (&dv)[M]) {
-    // one independent FMA chain per (axis, component) for ILP; summed at the end
+    // 2-D: one independent FMA chain per (axis, component) for ILP, summed at
+    // the end; 3-D: one chain per component (measured faster: fewer registers)
+    constexpr bool SPLIT = DIM == 2;
     double part[DIM][M];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
@@ -197,7 +199,7 @@ stp_picard_kernel(const StpArgs A) {
 #pragma unroll
       for (int k = 0; k < M; ++k) {
         const double* Fa = Fb + (a * M + k) * NPCP + pb[a];
-        double acc_ak = 0.0;
+        double acc_ak = (SPLIT || a == 0) ? 0.0 : part[a > 0 ? a - 1 : 0][k];
         if (a == DIM - 1 && (N % 2 == 0)) {
           // contiguous pencil: 16-byte pair loads (lanes of one pencil broadcast)
 #pragma unroll
@@ -216,10 +218,14 @@ stp_picard_kernel(const StpArgs A) {
     }
 #pragma unroll
     for (int k = 0; k < M; ++k) {
-      double v = part[0][k];
+      if (SPLIT) {
+        double v = part[0][k];
 #pragma unroll
-      for (int a = 1; a < DIM; ++a) v += part[a][k];
-      dv[k] = v;
+        for (int a = 1; a < DIM; ++a) v += part[a][k];
+        dv[k] = v;
+      } else {
+        dv[k] = part[DIM - 1][k];
+      }
     }
   };
 

@@ -126,7 +126,12 @@ template <int K>
 static int launch_fv_k(const FvArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
   const size_t smem = FvSmem<KIND, DIM, K>::BYTES;
-  auto kern = fv_patch_kernel<KIND, DIM, K>;
+  // EDG_FV_MINB=2 selects the 2-CTA/SM register budget (tuning knob)
+  static const int minb = [] {
+    const char* v = getenv("EDG_FV_MINB");
+    return v ? atoi(v) : 0;
+  }();
+  auto kern = (minb == 2) ? fv_patch_kernel<KIND, DIM, K, 2> : fv_patch_kernel<KIND, DIM, K>;
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
   if (a.npatches > 0) kern<<<a.npatches, FvCfg<DIM, K>::THREADS, smem, st>>>(a);
   return check_launch();
