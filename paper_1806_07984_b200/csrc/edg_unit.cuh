@@ -5,6 +5,7 @@
 #include <cstdlib>
 
 #include "edg_stp.cuh"
+#include "edg_stp_th.cuh"
 #include "edg_faces.cuh"
 #include "edg_fv.cuh"
 #include "edg_dt.cuh"
@@ -33,6 +34,23 @@ static int set_smem(K kernel, size_t bytes) {
 template <int N>
 static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  if constexpr (DIM == 2 && N % 2 == 0) {
+    // time-split kernel for even node counts (EDG_STP_TH=0 selects the
+    // one-thread-per-node kernel, tuning knob)
+    static const int th = [] {
+      const char* v = getenv("EDG_STP_TH");
+      return v ? atoi(v) : 1;
+    }();
+    if (th) {
+      using Ct = StpThCfg<DIM, N>;
+      const size_t smem = StpThSmem<KIND, DIM, N>::BYTES;
+      auto kern = stp_picard_th_kernel<KIND, DIM, N>;
+      if (set_smem(kern, smem)) return EDG_ERR_CUDA;
+      const int blocks = (a.nwork + Ct::CPB - 1) / Ct::CPB;
+      if (blocks > 0) kern<<<blocks, Ct::THREADS, smem, st>>>(a);
+      return check_launch();
+    }
+  }
   using Cf = StpCfg<DIM, N>;
   const size_t smem = StpSmem<KIND, DIM, N>::BYTES;
   // EDG_STP_MINB=2 selects the 2-CTA/SM register budget (no spills) instead
