@@ -22,11 +22,11 @@ struct StpThCfg {
   static constexpr int NF = ipow(N, DIM - 1);
   static constexpr int H = N / 2;
   // cells per CTA: ~128-160 nodes, a multiple of 16 nodes when possible
-  static constexpr int CPB = NPC >= 128 ? 1 : (NPC == 36 ? 4 : 128 / NPC);
+  static constexpr int CPB = NPC >= 64 ? 1 : (NPC == 36 ? 2 : 64 / NPC);
   static constexpr int NODES = CPB * NPC;
   static constexpr int WARPS = (NODES + 15) / 16;
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int MINB = 2;
+  static constexpr int MINB = 3;
 };
 
 template <int KIND, int DIM, int N>
