@@ -118,6 +118,14 @@ int edg_corrector(const edg_pde* pde, int32_t order, const double* basis_dev, in
                   double* q_out_dev, unsigned long long* dt_slots_dev, const double* hmin_dev,
                   uint32_t* status_dev, void* stream);
 
+/* Fused Cartesian corrector on a uniform row-major cells_per_axis^dim grid
+ * (periodic or outflow): neighbours by index arithmetic, no table. */
+int edg_corrector_grid(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t cells_per_axis,
+                       int32_t periodic, const double* q_end_dev, const double* trace_q_dev,
+                       const double* trace_f_dev, const double* edges_dev, double* q_out_dev,
+                       unsigned long long* dt_slots_dev, const double* hmin_dev, uint32_t* status_dev,
+                       void* stream);
+
 /* ---- admissible_dt (kernels.py:267-281) -----------------------------------
  * edg_cell_speed_reduce: per-cell lambda (max over axes of max over nodes,
  * NaN axes dropped like Python max) -> candidate h_c / ((2p+1) lambda_c) for
@@ -169,6 +177,11 @@ int edg_fv_patch_step(const edg_pde* pde, int32_t k, int32_t npatches, const dou
                       const int32_t* nbr_dev, const double* dt_dev, const double* edges_dev,
                       double* out_dev, unsigned long long* dt_slots_dev, double h_cell,
                       uint32_t* status_dev, void* stream);
+/* FV step on a row-major patches_per_axis^d patch grid (periodic or
+ * outflow): neighbour patches by index arithmetic, no table. */
+int edg_fv_grid_step(const edg_pde* pde, int32_t k, int32_t patches_per_axis, int32_t periodic,
+                     const double* patch_dev, const double* dt_dev, const double* edges_dev, double* out_dev,
+                     unsigned long long* dt_slots_dev, double h_cell, uint32_t* status_dev, void* stream);
 /* patch_boundary_layers (kernels.py:256-264): out (B, 2d, m, k^(d-1)). */
 int edg_patch_boundary_layers(int32_t dim, int32_t m, int32_t k, int32_t npatches,
                               const double* patch_dev, double* out_dev, void* stream);

@@ -42,6 +42,7 @@ SIGNATURES = {
     "edg_project_to_faces": (C.c_int, [I32, I32, I32, P, I32, P, P, P]),
     "edg_riemann_rusanov": (C.c_int, [PDEP, I32, I32, P, P, I32, I32, P, P]),
     "edg_corrector": (C.c_int, [PDEP, I32, P, I32, P, P, P, P, P, P, P, I32, P, P, P, P, P]),
+    "edg_corrector_grid": (C.c_int, [PDEP, I32, P, I32, I32, P, P, P, P, P, P, P, P, P]),
     "edg_cell_speed_reduce": (C.c_int, [PDEP, I32, I32, I32, P, P, I32, P, P]),
     "edg_dt_slots_reset": (C.c_int, [P, P]),
     "edg_dt_finalize": (C.c_int, [P, D, P, P, I32, P, P]),
@@ -50,6 +51,7 @@ SIGNATURES = {
     "edg_interpolate_face_trace": (C.c_int, [I32, I32, I32, P, I32, P, P, I32, P, P]),
     "edg_fv_patch_update": (C.c_int, [PDEP, I32, I32, P, P, P, P, P, P]),
     "edg_fv_patch_step": (C.c_int, [PDEP, I32, I32, P, P, P, P, P, P, D, P, P]),
+    "edg_fv_grid_step": (C.c_int, [PDEP, I32, I32, I32, P, P, P, P, P, D, P, P]),
     "edg_patch_boundary_layers": (C.c_int, [I32, I32, I32, I32, P, P, P]),
     "edg_stream_priority_range": (C.c_int, [C.POINTER(I32), C.POINTER(I32)]),
 }

@@ -150,6 +150,8 @@ int edg_corrector(const edg_pde* pde, int32_t order, const double* basis_dev, in
   a.trace_q = trace_q_dev;
   a.trace_f = trace_f_dev;
   a.nbr = nbr_dev;
+  a.grid_n = 0;
+  a.periodic = 0;
   a.side_face = side_face_dev;
   a.outcomes = outcomes_dev;
   a.edges = edges_dev;
@@ -160,6 +162,40 @@ int edg_corrector(const edg_pde* pde, int32_t order, const double* basis_dev, in
   a.status = status_dev;
   a.pp = params_of(pde);
   return cuda_status(u->corr(order + 1, fused, a, (cudaStream_t)stream));
+}
+
+int edg_corrector_grid(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t cells_per_axis,
+                       int32_t periodic, const double* q_end_dev, const double* trace_q_dev, const double* trace_f_dev,
+                       const double* edges_dev, double* q_out_dev, unsigned long long* dt_slots_dev,
+                       const double* hmin_dev, uint32_t* status_dev, void* stream) {
+  const Unit* u = find_unit(pde);
+  if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
+  if (order < 1 || order + 1 > u->max_n()) return fail(EDG_ERR_CONFIG, "polynomial order not built for this pde/dim");
+  if (cells_per_axis < 1 || !trace_q_dev) return fail(EDG_ERR_CONFIG, "grid corrector needs a grid and trace_q");
+  if (dt_slots_dev && !hmin_dev) return fail(EDG_ERR_CONFIG, "dt fusion needs hmin");
+  long long nc = 1;
+  for (int d = 0; d < pde->dim; ++d) nc *= cells_per_axis;
+  if (nc > 0x7fffffffLL) return fail(EDG_ERR_CONFIG, "grid too large");
+  CorrArgs a;
+  a.basis = basis_dev;
+  a.ncells = (int32_t)nc;
+  a.order = order;
+  a.q_end = q_end_dev;
+  a.trace_q = trace_q_dev;
+  a.trace_f = trace_f_dev;
+  a.nbr = nullptr;
+  a.grid_n = cells_per_axis;
+  a.periodic = periodic ? 1 : 0;
+  a.side_face = nullptr;
+  a.outcomes = nullptr;
+  a.edges = edges_dev;
+  a.edges_per_cell = 0;
+  a.q_out = q_out_dev;
+  a.dt_slots = dt_slots_dev;
+  a.hmin = hmin_dev;
+  a.status = status_dev;
+  a.pp = params_of(pde);
+  return cuda_status(u->corr(order + 1, true, a, (cudaStream_t)stream));
 }
 
 int edg_cell_speed_reduce(const edg_pde* pde, int32_t order, int32_t ncells, int32_t npts, const double* q_dev,
@@ -329,6 +365,30 @@ int edg_fv_patch_step(const edg_pde* pde, int32_t k, int32_t npatches, const dou
   a.npatches = npatches;
   a.patch = patch_dev;
   a.nbr = nbr_dev;
+  a.dt = dt_dev;
+  a.edges = edges_dev;
+  a.out = out_dev;
+  a.dt_slots = dt_slots_dev;
+  a.h_cell = h_cell;
+  a.status = status_dev;
+  a.pp = params_of(pde);
+  return cuda_status(u->fv(k, a, (cudaStream_t)stream));
+}
+
+int edg_fv_grid_step(const edg_pde* pde, int32_t k, int32_t patches_per_axis, int32_t periodic,
+                     const double* patch_dev, const double* dt_dev, const double* edges_dev, double* out_dev,
+                     unsigned long long* dt_slots_dev, double h_cell, uint32_t* status_dev, void* stream) {
+  const Unit* u = find_unit(pde);
+  if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
+  if (patches_per_axis < 1) return fail(EDG_ERR_CONFIG, "empty patch grid");
+  long long np = 1;
+  for (int d = 0; d < pde->dim; ++d) np *= patches_per_axis;
+  FvArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.npatches = (int32_t)np;
+  a.patch = patch_dev;
+  a.pgrid_n = patches_per_axis;
+  a.periodic = periodic ? 1 : 0;
   a.dt = dt_dev;
   a.edges = edges_dev;
   a.out = out_dev;

@@ -24,6 +24,8 @@ struct CorrArgs {
   const double* trace_q;
   const double* trace_f;
   const int32_t* nbr;
+  int32_t grid_n;           // > 0: uniform row-major grid_n^DIM mesh, neighbours by arithmetic
+  int32_t periodic;
   const int32_t* side_face;
   const double* outcomes;
   const double* edges;
@@ -89,44 +91,73 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       const double sg = s ? 1.0 : -1.0;
       sV[slot * 2 * DIM * N + i] = __ddiv_rn(__dmul_rn(sg, tr), __dmul_rn(A.basis[EDG_BASIS_W(N) + j], e[a]));
     }
-    // phase 1: jumps outcome - trace_f on the 2d faces
+    // phase 1: jumps outcome - trace_f on the 2d faces.  All global loads of
+    // a thread's (at most IPT) face points are issued before any arithmetic.
     const size_t tb = (size_t)cell * TRC;
-    for (int it = node; it < 2 * DIM * NF; it += NPC) {
-      const int fs = it / NF, f = it - fs * NF;
-      const int a = fs >> 1, s = fs & 1;
-      double out[M];
-      if (FUSED) {
-        const int nb = A.nbr[(size_t)cell * 2 * DIM + fs];
-        double mine[M], theirs[M];
+    constexpr int TOT = 2 * DIM * NF;
+    constexpr int IPT = (TOT + NPC - 1) / NPC;
+    double mine[IPT][M], theirs[IPT][M], tfv[IPT][M];
 #pragma unroll
-        for (int k = 0; k < M; ++k) mine[k] = A.trace_q[tb + ((size_t)fs * M + k) * NF + f];
-        if (nb >= 0) {
-          const size_t ob = (size_t)nb * TRC + ((size_t)(2 * a + (1 - s)) * M) * NF + f;
+    for (int i = 0; i < IPT; ++i) {
+      const int it = node + i * NPC;
+      if (it < TOT) {
+        const int fs = it / NF, f = it - fs * NF;
+        const int a = fs >> 1, s = fs & 1;
 #pragma unroll
-          for (int k = 0; k < M; ++k) theirs[k] = A.trace_q[ob + (size_t)k * NF];
+        for (int k = 0; k < M; ++k) tfv[i][k] = __ldg(A.trace_f + tb + ((size_t)fs * M + k) * NF + f);
+        if (FUSED) {
+          int nb;
+          if (A.grid_n > 0) {
+            // uniform row-major N^DIM grid: neighbour by index arithmetic
+            const int n = A.grid_n;
+            int stride = 1;
+            for (int t = DIM - 1; t > a; --t) stride *= n;
+            const int ia = (cell / stride) % n;
+            int j = ia + (s ? 1 : -1);
+            if (j < 0 || j >= n) j = A.periodic ? (j + n) % n : -1;
+            nb = j < 0 ? -1 : cell + (j - ia) * stride;
+          } else {
+            nb = __ldg(A.nbr + (size_t)cell * 2 * DIM + fs);
+          }
+#pragma unroll
+          for (int k = 0; k < M; ++k) mine[i][k] = __ldg(A.trace_q + tb + ((size_t)fs * M + k) * NF + f);
+          const size_t ob = nb >= 0 ? (size_t)nb * TRC + ((size_t)(2 * a + (1 - s)) * M) * NF + f
+                                    : tb + ((size_t)fs * M) * NF + f;   // outflow ghost = own trace
+#pragma unroll
+          for (int k = 0; k < M; ++k) theirs[i][k] = __ldg(A.trace_q + ob + (size_t)k * NF);
         } else {
+          const int fidx = __ldg(A.side_face + (size_t)cell * 2 * DIM + fs);
+          if (fidx < 0) {
+            atomicOr(A.status, 2u);
 #pragma unroll
-          for (int k = 0; k < M; ++k) theirs[k] = mine[k];   // outflow ghost = own trace
-        }
-        // face oriented along +a: lo = lower cell's (a,1) trace, hi = upper cell's (a,0)
-        if (s == 1)
-          rusanov<KIND, DIM>(mine, theirs, a, 1, A.pp, out);
-        else
-          rusanov<KIND, DIM>(theirs, mine, a, 1, A.pp, out);
-      } else {
-        const int fidx = A.side_face[(size_t)cell * 2 * DIM + fs];
-        if (fidx < 0) {
-          atomicOr(A.status, 2u);
+            for (int k = 0; k < M; ++k) mine[i][k] = __longlong_as_double(0x7FF8000000000000ll);
+          } else {
 #pragma unroll
-          for (int k = 0; k < M; ++k) out[k] = __longlong_as_double(0x7FF8000000000000ll);
-        } else {
-#pragma unroll
-          for (int k = 0; k < M; ++k) out[k] = A.outcomes[((size_t)fidx * M + k) * NF + f];
+            for (int k = 0; k < M; ++k) mine[i][k] = __ldg(A.outcomes + ((size_t)fidx * M + k) * NF + f);
+          }
         }
       }
+    }
 #pragma unroll
-      for (int k = 0; k < M; ++k)
-        sJump[slot * TRC + (fs * M + k) * NF + f] = __dsub_rn(out[k], A.trace_f[tb + ((size_t)fs * M + k) * NF + f]);
+    for (int i = 0; i < IPT; ++i) {
+      const int it = node + i * NPC;
+      if (it < TOT) {
+        const int fs = it / NF, f = it - fs * NF;
+        const int a = fs >> 1, s = fs & 1;
+        double out[M];
+        if (FUSED) {
+          // face oriented along +a: lo = lower cell's (a,1) trace, hi = upper cell's (a,0)
+          if (s == 1)
+            rusanov<KIND, DIM>(mine[i], theirs[i], a, 1, A.pp, out);
+          else
+            rusanov<KIND, DIM>(theirs[i], mine[i], a, 1, A.pp, out);
+        } else {
+#pragma unroll
+          for (int k = 0; k < M; ++k) out[k] = mine[i][k];
+        }
+#pragma unroll
+        for (int k = 0; k < M; ++k) sJump[slot * TRC + (fs * M + k) * NF + f] = __dsub_rn(out[k], tfv[i][k]);
+      }
     }
   }
   __syncthreads();

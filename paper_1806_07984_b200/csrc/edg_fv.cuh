@@ -27,7 +27,9 @@ namespace edg {
 struct FvArgs {
   int32_t npatches;
   const double* patch;     // [B][M][k^d]
-  const int32_t* nbr;      // [B][2d] or null (halos given)
+  const int32_t* nbr;      // [B][2d] or null (halos given / grid)
+  int32_t pgrid_n;         // > 0: row-major pgrid_n^d patch grid, neighbours by arithmetic
+  int32_t periodic;
   const double* halos;     // [B][2d][M][k^(d-1)] or null
   const double* dt;
   const double* edges;     // [d] patch extent
@@ -131,45 +133,71 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
     }
   };
 
-  // ---- interior states: thread = volume ----
-  for (int c = tid; c < NC; c += THREADS) {
-    double q[M];
+  // ---- stage interior and halo states; every global load of a thread is
+  // issued before the first shared-memory store ----
+  constexpr int NIT = (NC + THREADS - 1) / THREADS;
+  constexpr int NHT = (2 * DIM * NL + THREADS - 1) / THREADS;
+  double qi_[NIT][M], qh_[NHT][M];
+  int xh_[NHT];
 #pragma unroll
-    for (int k = 0; k < M; ++k) q[k] = __ldg(src + k * NC + c);
-    stage(ext_of_cell(c), q);
+  for (int u = 0; u < NIT; ++u) {
+    const int c = tid + u * THREADS;
+#pragma unroll
+    for (int k = 0; k < M; ++k) qi_[u][k] = c < NC ? __ldg(src + k * NC + c) : 0.0;
   }
-  // ---- halo states: thread = one point of a face layer ----
-  for (int i = tid; i < 2 * DIM * NL; i += THREADS) {
-    const int fs = i / NL, f = i - fs * NL;
-    const int a = fs >> 1, s = fs & 1;
-    int e[DIM], t = f;
 #pragma unroll
-    for (int ax = DIM - 1; ax >= 0; --ax) {
-      if (ax == a) continue;
-      e[ax] = t % K;
-      t /= K;
+  for (int u = 0; u < NHT; ++u) {
+    const int i = tid + u * THREADS;
+    xh_[u] = -1;
+    if (i < 2 * DIM * NL) {
+      const int fs = i / NL, f = i - fs * NL;
+      const int a = fs >> 1, s = fs & 1;
+      int e[DIM], t = f;
+#pragma unroll
+      for (int ax = DIM - 1; ax >= 0; --ax) {
+        if (ax == a) continue;
+        e[ax] = t % K;
+        t /= K;
+      }
+      int x = 0;
+#pragma unroll
+      for (int ax = 0; ax < DIM; ++ax) x += (ax == a ? (s ? K + 1 : 0) : e[ax] + 1) * estride(ax);
+      xh_[u] = x;
+      if (A.halos) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) qh_[u][k] = __ldg(A.halos + (((size_t)b * 2 * DIM + fs) * M + k) * NL + f);
+      } else {
+        int nb;
+        if (A.pgrid_n > 0) {
+          // Cartesian patch grid (row-major): neighbour patch by index arithmetic
+          const int n = A.pgrid_n;
+          int stride = 1;
+          for (int ax = DIM - 1; ax > a; --ax) stride *= n;
+          const int ia = (b / stride) % n;
+          int j = ia + (s ? 1 : -1);
+          if (j < 0 || j >= n) j = A.periodic ? (j + n) % n : -1;
+          nb = j < 0 ? -1 : b + (j - ia) * stride;
+        } else {
+          nb = __ldg(A.nbr + (size_t)b * 2 * DIM + fs);
+        }
+        // neighbour below (s=0) contributes its last layer, above its first;
+        // outflow (-1): own layer on that side
+        e[a] = nb >= 0 ? (s == 0 ? K - 1 : 0) : (s == 0 ? 0 : K - 1);
+        int c = 0;
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) c = c * K + e[ax];
+        const double* ps = A.patch + (size_t)(nb >= 0 ? nb : b) * M * NC + c;
+#pragma unroll
+        for (int k = 0; k < M; ++k) qh_[u][k] = __ldg(ps + k * NC);
+      }
     }
-    double q[M];
-    if (A.halos) {
-#pragma unroll
-      for (int k = 0; k < M; ++k) q[k] = __ldg(A.halos + (((size_t)b * 2 * DIM + fs) * M + k) * NL + f);
-    } else {
-      const int nb = A.nbr[(size_t)b * 2 * DIM + fs];
-      // neighbour below (s=0) contributes its last layer, above its first;
-      // outflow (-1): own layer on that side
-      e[a] = nb >= 0 ? (s == 0 ? K - 1 : 0) : (s == 0 ? 0 : K - 1);
-      int c = 0;
-#pragma unroll
-      for (int ax = 0; ax < DIM; ++ax) c = c * K + e[ax];
-      const double* ps = A.patch + (size_t)(nb >= 0 ? nb : b) * M * NC + c;
-#pragma unroll
-      for (int k = 0; k < M; ++k) q[k] = __ldg(ps + k * NC);
-    }
-    int x = 0;
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) x += (ax == a ? (s ? K + 1 : 0) : e[ax] + 1) * estride(ax);
-    stage(x, q);
   }
+#pragma unroll
+  for (int u = 0; u < NIT; ++u)
+    if (tid + u * THREADS < NC) stage(ext_of_cell(tid + u * THREADS), qi_[u]);
+#pragma unroll
+  for (int u = 0; u < NHT; ++u)
+    if (xh_[u] >= 0) stage(xh_[u], qh_[u]);
   const double dt = *A.dt;
   __syncthreads();
 

@@ -35,11 +35,11 @@ template <int N>
 static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
   if constexpr (DIM == 2 && N % 2 == 0) {
-    // time-split kernel for even node counts (EDG_STP_TH=0 selects the
-    // one-thread-per-node kernel, tuning knob)
+    // time-split kernel for even node counts: opt-in (EDG_STP_TH=1); measured
+    // 10-15% slower than the one-thread-per-node kernel on cfg2 / cfg5
     static const int th = [] {
       const char* v = getenv("EDG_STP_TH");
-      return v ? atoi(v) : 1;
+      return v ? atoi(v) : 0;
     }();
     if (th) {
       using Ct = StpThCfg<DIM, N>;

@@ -259,11 +259,11 @@ class DGSolver(_Base):
             if tm:
                 tm.end("stp")
                 tm.begin("corrector")
-            _lib.check(lib.edg_corrector(C.byref(self.native), self.order, _lib.ptr(self.table), self.ncells,
-                                         _lib.ptr(self.q_end), _lib.ptr(self.trace_q), _lib.ptr(self.trace_f),
-                                         _lib.ptr(self.nbr), None, None, _lib.ptr(self.edges), self.edges_per_cell,
-                                         _lib.ptr(self.Qn), _lib.ptr(self.slots), _lib.ptr(self.hmin),
-                                         _lib.ptr(self.status), _stream()), "corrector")
+            _lib.check(lib.edg_corrector_grid(C.byref(self.native), self.order, _lib.ptr(self.table), self.mesh.N,
+                                              int(self.mesh.periodic), _lib.ptr(self.q_end), _lib.ptr(self.trace_q),
+                                              _lib.ptr(self.trace_f), _lib.ptr(self.edges), _lib.ptr(self.Qn),
+                                              _lib.ptr(self.slots), _lib.ptr(self.hmin), _lib.ptr(self.status),
+                                              _stream()), "corrector")
             if tm:
                 tm.end("corrector")
             _lib.check(lib.edg_order_by_iterations(self.ncells, _lib.ptr(self.iterations), _lib.ptr(self.work_order),
@@ -348,10 +348,10 @@ class FVSolver(_Base):
         tm = self.kernel_timer
         if tm:
             tm.begin("fv")
-        _lib.check(lib.edg_fv_patch_step(C.byref(self.native), self.k, self.npatches, _lib.ptr(self.Q),
-                                         _lib.ptr(self.nbr), _lib.ptr(self.dt), _lib.ptr(self.edges),
-                                         _lib.ptr(self.Qn), _lib.ptr(self.slots), self.h_cell,
-                                         _lib.ptr(self.status), _stream()), "fv_patch_step")
+        _lib.check(lib.edg_fv_grid_step(C.byref(self.native), self.k, self.pmesh.N, int(self.pmesh.periodic),
+                                        _lib.ptr(self.Q), _lib.ptr(self.dt), _lib.ptr(self.edges),
+                                        _lib.ptr(self.Qn), _lib.ptr(self.slots), self.h_cell,
+                                        _lib.ptr(self.status), _stream()), "fv_patch_step")
         if tm:
             tm.end("fv")
         self.Q, self.Qn = self.Qn, self.Q
