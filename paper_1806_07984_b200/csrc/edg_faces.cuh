@@ -96,10 +96,15 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
     const size_t tb = (size_t)cell * TRC;
     constexpr int TOT = 2 * DIM * NF;
     constexpr int IPT = (TOT + NPC - 1) / NPC;
-    double mine[IPT][M], theirs[IPT][M], tfv[IPT][M];
+    // hoist all items of a thread when that costs few registers; otherwise one
+    // item at a time (3-D p=4: hoisting two items lost occupancy, measured)
+    constexpr int GRP = (3 * M * IPT <= 24) ? IPT : 1;
+#pragma unroll 1
+    for (int g0 = 0; g0 < IPT; g0 += GRP) {
+    double mine[GRP][M], theirs[GRP][M], tfv[GRP][M];
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const int it = node + i * NPC;
+    for (int i = 0; i < GRP; ++i) {
+      const int it = node + (g0 + i) * NPC;
       if (it < TOT) {
         const int fs = it / NF, f = it - fs * NF;
         const int a = fs >> 1, s = fs & 1;
@@ -139,8 +144,8 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       }
     }
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const int it = node + i * NPC;
+    for (int i = 0; i < GRP; ++i) {
+      const int it = node + (g0 + i) * NPC;
       if (it < TOT) {
         const int fs = it / NF, f = it - fs * NF;
         const int a = fs >> 1, s = fs & 1;
@@ -158,6 +163,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
 #pragma unroll
         for (int k = 0; k < M; ++k) sJump[slot * TRC + (fs * M + k) * NF + f] = __dsub_rn(out[k], tfv[i][k]);
       }
+    }
     }
   }
   __syncthreads();
