@@ -58,6 +58,20 @@ constexpr int stp_best_cpb(int npc, int target) {
   return best;
 }
 
+// Lane -> node map of the 3-D p = 4 kernel (one 125-node cell per 128-thread
+// CTA).  Warp w takes a compact block of (i1, i2) pencil pairs with all five
+// i0 values, so that a warp-wide LDS.64 of a derivative step touches <= 16
+// distinct pencils (one wavefront) on all three axes for warps 0-2 (warp 3:
+// two on axis 1) instead of 25 distinct axis-0 pencils in row-major order
+// (generated and checked by tools/perm3d5.py; -1 = idle lane).
+static __constant__ int kStpPerm3d5[128] = {
+    0,  25, 50, 75, 100, 1,  26, 51, 76, 101, 2,   27, 52, 77, 102, 5,  30, 55, 80, 105, 6,  31,
+    56, 81, 106, 7,  32, 57, 82, 107, 20, 45, 10,  35, 60, 85, 110, 11, 36, 61, 86, 111, 12, 37,
+    62, 87, 112, 15, 40, 65, 90, 115, 16, 41, 66,  91, 116, 17, 42, 67, 92, 117, 70, 95, 3,  28,
+    53, 78, 103, 4,  29, 54, 79, 104, 8,  33, 58,  83, 108, 9,  34, 59, 84, 109, 13, 38, 63, 88,
+    113, 14, 39, 64, 89, 114, 120, -1, 18, 43, 68, 93, 118, 19, 44, 69, 94, 119, 23, 48, 73, 98,
+    123, 24, 49, 74, 99, 124, 21, 46, 71, 96, 121, 22, 47, 72, 97, 122, -1, -1};
+
 template <int DIM, int N>
 struct StpCfg {
   static constexpr int NPC = ipow(N, DIM);
@@ -110,10 +124,21 @@ stp_picard_kernel(const StpArgs A) {
   unsigned long long* sRed = reinterpret_cast<unsigned long long*>(sF + 2 * Sm::FB);   // [2][CPB]
 
   const int tid = threadIdx.x;
-  const int slot = tid / NPC;
-  const int node = tid - slot * NPC;
+  int slot, node;
+  bool lane_ok;
+  if constexpr (DIM == 3 && N == 5 && CPB == 1) {
+    // compact lane->node blocks: <= 16 distinct pencils per warp on most axes
+    const int v = kStpPerm3d5[tid];
+    slot = 0;
+    node = v < 0 ? 0 : v;
+    lane_ok = v >= 0;
+  } else {
+    slot = tid / NPC;
+    node = tid - slot * NPC;
+    lane_ok = slot < CPB;
+  }
   const int item = blockIdx.x * CPB + slot;
-  const bool has_cell = (slot < CPB) && (item < A.nwork);
+  const bool has_cell = lane_ok && (item < A.nwork);
   const int cell = has_cell ? (A.cell_list ? __ldg(A.cell_list + item) : item) : 0;
   const double dt = *A.dt;
 
@@ -286,7 +311,7 @@ stp_picard_kernel(const StpArgs A) {
           qh[r][k] = acc[r][k];
         }
     }
-    seg_max_atomic(red, slot < CPB ? slot : -1, mk);
+    seg_max_atomic(red, lane_ok ? slot : -1, mk);
     __syncthreads();
     if (active) {
       its = it;
