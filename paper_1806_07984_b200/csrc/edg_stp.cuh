@@ -126,7 +126,10 @@ stp_picard_kernel(const StpArgs A) {
   const int tid = threadIdx.x;
   int slot, node;
   bool lane_ok;
-  if constexpr (DIM == 3 && N == 5 && CPB == 1) {
+  // disabled: measured 20% slower on cfg3 (bank conflicts of the compact
+  // blocks outweigh the fewer distinct pencils); kept for reference
+  constexpr bool kUsePerm3d5 = false;
+  if constexpr (kUsePerm3d5 && DIM == 3 && N == 5 && CPB == 1) {
     // compact lane->node blocks: <= 16 distinct pencils per warp on most axes
     const int v = kStpPerm3d5[tid];
     slot = 0;
