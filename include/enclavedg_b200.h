@@ -82,6 +82,15 @@ int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev,
                    double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev,
                    unsigned long long* iter_total_dev, void* stream);
 
+/* ---- stp_linear (kernels.py:82-106): Cauchy-Kowalevski predictor of a
+ * linear PDE (advection); other PDEs -> EDG_ERR_NO_SPEED (EnclaveDgError
+ * "stp_linear requires a linear flux").  Same buffers as edg_stp_picard;
+ * trace_f = F(trace_q) pointwise as in the reference. */
+int edg_stp_linear(const edg_pde* pde, int32_t order, const double* basis_dev, const double* q_dev,
+                   const int32_t* cell_list_dev, int32_t nwork, const double* edges_dev, int32_t edges_per_cell,
+                   const double* dt_dev, double* q_end_dev, double* q_int_dev, double* trace_q_dev,
+                   double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev, void* stream);
+
 /* Work ordering for the next predictor launch: order_dev = the cells sorted
  * by descending Picard count (counting sort, 3 small kernels).  scratch_dev:
  * 128 int32, zero-initialised once by the caller. */

@@ -13,6 +13,7 @@
 namespace edg {
 #define EDG_DECL_UNIT(name)                                                                                  \
   int unit_##name##_stp(int n, const StpArgs& a, cudaStream_t st);                                           \
+  int unit_##name##_stl(int n, const StpArgs& a, cudaStream_t st);                                           \
   int unit_##name##_corr(int n, bool fused, const CorrArgs& a, cudaStream_t st);                             \
   int unit_##name##_faces(int n, const FaceArgs& a, cudaStream_t st);                                        \
   int unit_##name##_speed(int order, int ncells, int npts, const double* q, const double* hmin, int h_per_cell, \
@@ -30,6 +31,7 @@ EDG_DECL_UNIT(euler3)
 
 struct Unit {
   int (*stp)(int, const StpArgs&, cudaStream_t);
+  int (*stl)(int, const StpArgs&, cudaStream_t);
   int (*corr)(int, bool, const CorrArgs&, cudaStream_t);
   int (*faces)(int, const FaceArgs&, cudaStream_t);
   int (*speed)(int, int, int, const double*, const double*, int, unsigned long long*, const PdeParams&, cudaStream_t);
@@ -38,7 +40,7 @@ struct Unit {
   int (*max_n)();
 };
 #define EDG_UNIT(name) \
-  Unit { unit_##name##_stp, unit_##name##_corr, unit_##name##_faces, unit_##name##_speed, unit_##name##_riemann, unit_##name##_fv, unit_##name##_max_n }
+  Unit { unit_##name##_stp, unit_##name##_stl, unit_##name##_corr, unit_##name##_faces, unit_##name##_speed, unit_##name##_riemann, unit_##name##_fv, unit_##name##_max_n }
 
 static const Unit* find_unit(const edg_pde* p) {
   static const Unit units[3][2] = {{EDG_UNIT(advection2), EDG_UNIT(advection3)},
@@ -120,6 +122,34 @@ int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev, c
   a.converged = converged_dev;
   a.iter_total = iter_total_dev;
   return cuda_status(u->stp(order + 1, a, (cudaStream_t)stream));
+}
+
+int edg_stp_linear(const edg_pde* pde, int32_t order, const double* basis_dev, const double* q_dev,
+                   const int32_t* cell_list_dev, int32_t nwork, const double* edges_dev, int32_t edges_per_cell,
+                   const double* dt_dev, double* q_end_dev, double* q_int_dev, double* trace_q_dev,
+                   double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev, void* stream) {
+  const Unit* u = find_unit(pde);
+  if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
+  if (pde->kind != EDG_PDE_ADVECTION) return fail(EDG_ERR_NO_SPEED, "stp_linear requires a linear flux");
+  if (order < 1 || order + 1 > u->max_n()) return fail(EDG_ERR_CONFIG, "polynomial order not built for this pde/dim");
+  if (nwork <= 0) return EDG_OK;
+  StpArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.q = q_dev;
+  a.cell_list = cell_list_dev;
+  a.nwork = nwork;
+  a.basis = basis_dev;
+  a.edges = edges_dev;
+  a.edges_per_cell = edges_per_cell;
+  a.dt = dt_dev;
+  a.pp = params_of(pde);
+  a.q_end = q_end_dev;
+  a.q_int = q_int_dev;
+  a.trace_q = trace_q_dev;
+  a.trace_f = trace_f_dev;
+  a.iterations = iterations_dev;
+  a.converged = converged_dev;
+  return cuda_status(u->stl(order + 1, a, (cudaStream_t)stream));
 }
 
 int edg_riemann_rusanov(const edg_pde* pde, int32_t nfaces, int32_t npts, const double* lo_dev,

@@ -247,6 +247,9 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
   }
 
   // ---- write back, non-finite count, next-step dt candidate ----
+  unsigned long long lk[DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) lk[a] = 0ull;
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
     const int c = c0 + j;
@@ -258,14 +261,26 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
         finite = finite && (fabs(o[j][k]) <= 1.7976931348623157e308);
       }
       if (A.status && !finite) atomicAdd(A.status + 1, 1u);
+      if (A.dt_slots) {
+        const auto pr = P::parts(o[j], A.pp);
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          const unsigned long long key = maxkey(P::lam(o[j], pr, a, A.pp));
+          lk[a] = key > lk[a] ? key : lk[a];
+        }
+      }
     }
-    if (A.dt_slots) {
-      unsigned long long lk[DIM];
-      const auto pr = P::parts(o[j], A.pp);
+  }
+  if (A.dt_slots) {
+    // whole CTA is one patch: butterfly max over the warp, one atomic per warp and axis
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) lk[a] = ok ? maxkey(P::lam(o[j], pr, a, A.pp)) : 0ull;
+    for (int a = 0; a < DIM; ++a) {
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) seg_max_atomic(sLam + a, 0, lk[a]);
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, lk[a], off);
+        lk[a] = v > lk[a] ? v : lk[a];
+      }
+      if ((tid & 31) == 0 && lk[a]) atomicMax(sLam + a, lk[a]);
     }
   }
   if (A.dt_slots) {

@@ -76,7 +76,9 @@ template <int DIM, int N>
 struct StpCfg {
   static constexpr int NPC = ipow(N, DIM);
   static constexpr int NF = ipow(N, DIM - 1);
-  static constexpr int TARGET = 128;
+  // 2-D: ~192 threads (cfg2: 5 cells = 180 nodes, two CTAs = 12 warps fill the
+  // 168-register budget of an SM); 3-D: one 125-node cell per 128 threads
+  static constexpr int TARGET = DIM == 2 ? 160 : 128;
   static constexpr int CPB = stp_best_cpb(NPC, TARGET);
   static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32;
   // resident CTAs per SM requested from ptxas (caps registers per thread)

@@ -6,6 +6,7 @@
 
 #include "edg_stp.cuh"
 #include "edg_stp_th.cuh"
+#include "edg_stp_ck.cuh"
 #include "edg_faces.cuh"
 #include "edg_fv.cuh"
 #include "edg_dt.cuh"
@@ -64,6 +65,33 @@ static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
   const int blocks = (a.nwork + Cf::CPB - 1) / Cf::CPB;
   if (blocks > 0) kern<<<blocks, Cf::THREADS, smem, st>>>(a);
   return check_launch();
+}
+
+template <int N>
+static int launch_stl_n(const StpArgs& a, cudaStream_t st) {
+  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  if constexpr (KIND != EDG_PDE_ADVECTION) {
+    return EDG_ERR_NO_SPEED;   // EnclaveDgError: stp_linear requires a linear flux (kernels.py:89-90)
+  } else {
+    using Cf = StpCfg<DIM, N>;
+    const size_t smem = sizeof(double) * (N * N + 2 * N + 1 + Cf::CPB * DIM * Pde<KIND, DIM>::M * Cf::NPC);
+    auto kern = stp_linear_kernel<KIND, DIM, N>;
+    if (set_smem(kern, smem)) return EDG_ERR_CUDA;
+    const int blocks = (a.nwork + Cf::CPB - 1) / Cf::CPB;
+    if (blocks > 0) kern<<<blocks, Cf::THREADS, smem, st>>>(a);
+    return check_launch();
+  }
+}
+
+int EDG_FN(_stl)(int n, const StpArgs& a, cudaStream_t st) {
+  switch (n) {
+#define EDG_CASE(NN) \
+  case NN:           \
+    return launch_stl_n<NN>(a, st);
+    EDG_FOR_N(EDG_CASE)
+#undef EDG_CASE
+  }
+  return EDG_ERR_CONFIG;
 }
 
 int EDG_FN(_stp)(int n, const StpArgs& a, cudaStream_t st) {

@@ -154,6 +154,44 @@ def stp_picard(q, pde: PdeDescriptor, dt, basis: PolynomialBasis, edges, tol=1e-
                           iterations=int(r["iterations"][0]), converged=bool(r["converged"][0]))
 
 
+def stp_linear_batch(Q, pde: PdeDescriptor, dt, basis: PolynomialBasis, edges, cell_list=None):
+    """Cauchy-Kowalevski predictor of many cells (kernels.py:82-106 per cell);
+    same outputs as stp_picard_batch (iterations 0, converged 1)."""
+    torch = _torch()
+    if not pde.is_linear:
+        raise EnclaveDgError("stp_linear requires a linear flux")
+    _check_supported(pde, basis.order)
+    Qd, _ = _dev(Q)
+    C_ = Qd.shape[0]
+    d, m, n = pde.dim, pde.m, basis.n
+    out = dict(q_end=torch.empty_like(Qd), q_int=torch.empty_like(Qd),
+               trace_q=torch.empty((C_, 2 * d, m) + (n,) * (d - 1), dtype=torch.float64, device="cuda"),
+               trace_f=torch.empty((C_, 2 * d, m) + (n,) * (d - 1), dtype=torch.float64, device="cuda"),
+               iterations=torch.zeros(C_, dtype=torch.int32, device="cuda"),
+               converged=torch.zeros(C_, dtype=torch.uint8, device="cuda"))
+    e, per = _edges_dev(edges, d, C_)
+    dtd = _scalar_dev(dt)
+    nwork = C_ if cell_list is None else int(cell_list.numel())
+    st = _lib.load().edg_stp_linear(C.byref(pde.native()), basis.order, _lib.ptr(basis.device_table()),
+                                    _lib.ptr(Qd), _lib.ptr(cell_list), nwork, _lib.ptr(e), per, _lib.ptr(dtd),
+                                    _lib.ptr(out["q_end"]), _lib.ptr(out["q_int"]), _lib.ptr(out["trace_q"]),
+                                    _lib.ptr(out["trace_f"]), _lib.ptr(out["iterations"]), _lib.ptr(out["converged"]),
+                                    _stream())
+    _lib.check(st, "stp_linear")
+    return out
+
+
+def stp_linear(q, pde: PdeDescriptor, dt, basis: PolynomialBasis, edges) -> PredictorStore:
+    """Drop-in for kernels.py:82-106 on one cell."""
+    Qd, host = _dev(q)
+    r = stp_linear_batch(Qd[None], pde, dt, basis, tuple(edges))
+    conv = lambda t: t.cpu().numpy() if host else t  # noqa: E731
+    keys = trace_keys(pde.dim)
+    return PredictorStore(conv(r["q_int"][0]), conv(r["q_end"][0]),
+                          {k: conv(r["trace_q"][0, j]) for j, k in enumerate(keys)},
+                          {k: conv(r["trace_f"][0, j]) for j, k in enumerate(keys)})
+
+
 def project_to_faces_batch(V, basis: PolynomialBasis, dim: int):
     torch = _torch()
     Vd, _ = _dev(V)

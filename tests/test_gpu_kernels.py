@@ -199,3 +199,17 @@ def test_grid_and_table_paths_agree_bitwise(edg):
     out = edg.kernels.fv_patch_update_batch(torch.from_numpy(P0).cuda(), f.pde, f.dt_hist[0:1], (0.5, 0.5, 0.5),
                                             nbr=f.nbr)
     assert torch.equal(out, f.state())
+
+
+def test_stp_linear_vs_reference_ck_vectors(edg, golden_ops):
+    """stp_linear (kernels.py:82-106) against the reference's CK outputs."""
+    for ci in (0, 5):
+        g = lambda k: golden_ops[f"stp{ci}_{k}"]  # noqa: E731
+        dim, p, code = (int(v) for v in g("meta"))
+        pde = edg.pde.advection((1.0, 0.5, 0.25)[:dim], dim)
+        for c in range(g("q").shape[0]):
+            st = edg.kernels.stp_linear(g("q")[c], pde, float(g("dt")), edg.basis.get_basis(p), tuple(g("edges")))
+            assert rel_linf(st.q_end, g("ck_q_end")[c]) < 1e-12
+            assert rel_linf(st.q_int, g("ck_q_int")[c]) < 1e-12
+    with pytest.raises(edg.errors.EnclaveDgError):
+        edg.kernels.stp_linear(np.ones((4, 4, 4)), edg.pde.euler(2), 1e-3, edg.basis.get_basis(3), (0.1, 0.1))
