@@ -78,7 +78,7 @@ struct StpCfg {
   static constexpr int NF = ipow(N, DIM - 1);
   // 2-D: ~192 threads (cfg2: 5 cells = 180 nodes, two CTAs = 12 warps fill the
   // 168-register budget of an SM); 3-D: one 125-node cell per 128 threads
-  static constexpr int TARGET = DIM == 2 ? 160 : 128;
+  static constexpr int TARGET = 128;
   static constexpr int CPB = stp_best_cpb(NPC, TARGET);
   static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32;
   // resident CTAs per SM requested from ptxas (caps registers per thread)
@@ -96,7 +96,13 @@ struct StpSmem {
   static constexpr int NP = N;   // (padding odd N to N+1 for pair loads measured slower on 3-D p=4)
   static constexpr int NPCP = C::NPC / N * NP;
   static constexpr int FB = C::CPB * DIM * M * NPCP;            // one flux buffer
-  static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * FB) + sizeof(unsigned long long) * 2 * C::CPB;
+  // time nodes per pipeline stage (one barrier per stage); EDG_STP_G overrides
+#ifdef EDG_STP_G
+  static constexpr int G = EDG_STP_G;
+#else
+  static constexpr int G = DIM == 2 ? 2 : 1;
+#endif
+  static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * G * FB) + sizeof(unsigned long long) * 2 * C::CPB;
 };
 
 template <int KIND, int DIM, int N, int MINB = StpCfg<DIM, N>::MINB>
@@ -123,7 +129,7 @@ stp_picard_kernel(const StpArgs A) {
   double* sBs = sC + N;              // sum_s B[r][s]
   double* sF = smem + Sm::OPS;       // flux buffers [2][CPB][DIM][M][NPCP], 16-byte aligned (OPS even)
   static_assert(Sm::OPS % 2 == 0 && Sm::OPS >= 2 * N * N + 5 * N, "operator block must keep sF 16-byte aligned");
-  unsigned long long* sRed = reinterpret_cast<unsigned long long*>(sF + 2 * Sm::FB);   // [2][CPB]
+  unsigned long long* sRed = reinterpret_cast<unsigned long long*>(sF + 2 * Sm::G * Sm::FB);   // [2][CPB]
 
   const int tid = threadIdx.x;
   int slot, node;
@@ -276,6 +282,9 @@ stp_picard_kernel(const StpArgs A) {
         }
       }
     } else {
+      // G time nodes per barrier; stage buffers [2][G]
+      constexpr int G = Sm::G;
+      auto slotbuf = [&](int stage, int g) { return buf0 + (stage * G + g) * Sm::FB; };
       if (active) {
 #pragma unroll
         for (int k = 0; k < M; ++k) {
@@ -283,22 +292,33 @@ stp_picard_kernel(const StpArgs A) {
 #pragma unroll
           for (int r = 0; r < N; ++r) acc[r][k] = sC[r] * q0;
         }
-        put_flux(buf0, qh[0]);
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (g < N) put_flux(slotbuf(0, g), qh[g]);
       }
       __syncthreads();
-      // software pipeline: the flux of time node s+1 is evaluated and stored
-      // (other buffer) while the derivative of time node s is contracted
+      // software pipeline: the fluxes of the next G time nodes are evaluated
+      // and stored (other stage) while the derivatives of this group are
+      // contracted; one barrier per group
 #pragma unroll
-      for (int s = 0; s < N; ++s) {
+      for (int s0 = 0; s0 < N; s0 += G) {
+        const int stage = (s0 / G) & 1;
         if (active) {
-          if (s + 1 < N) put_flux(((s + 1) & 1) ? buf1 : buf0, qh[s + 1]);
-          double dv[M];
-          deriv((s & 1) ? buf1 : buf0, dv);
 #pragma unroll
-          for (int r = 0; r < N; ++r) {
-            const double b = sB[r * N + s];
+          for (int g = 0; g < G; ++g)
+            if (s0 + G + g < N) put_flux(slotbuf(stage ^ 1, g), qh[s0 + G + g]);
 #pragma unroll
-            for (int k = 0; k < M; ++k) acc[r][k] = fma(b, dv[k], acc[r][k]);
+          for (int g = 0; g < G; ++g) {
+            if (s0 + g < N) {
+              double dv[M];
+              deriv(slotbuf(stage, g), dv);
+#pragma unroll
+              for (int r = 0; r < N; ++r) {
+                const double b = sB[r * N + s0 + g];
+#pragma unroll
+                for (int k = 0; k < M; ++k) acc[r][k] = fma(b, dv[k], acc[r][k]);
+              }
+            }
           }
         }
         __syncthreads();
@@ -382,29 +402,36 @@ stp_picard_kernel(const StpArgs A) {
       for (int k = 0; k < M; ++k) St[((1 + a) * M + k) * NPC + node] = fi[a][k] * dt;
   }
   __syncthreads();
-  if (has_cell) {
-    // outputs: family (trace_q from q_int, trace_f from fint_a) x face (a, s) x k x f
+  // face projections, one task per (axis a, pencil f): the thread loads the
+  // pencil of q_int and of fint_a once and writes both sides of both families
+  // (trace_q / trace_f (a, 0) and (a, 1)) for all components
+  constexpr int TASKS = DIM * NF;
+  for (int task = node; has_cell && task < TASKS; task += NPC) {
     constexpr int PER_FAM = 2 * DIM * M * NF;
     const size_t tbase = (size_t)cell * PER_FAM;
+    const int a = task / NF, f = task - a * NF;
+    const int st = a == DIM - 1 ? 1 : ipow(N, DIM - 1 - a);
+    const int hi = f / st, lo = f - hi * st;
+    const int base = hi * st * N + lo;
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-      constexpr int dummy = 0;
-      (void)dummy;
-      const int st = ipow(N, DIM - 1 - a);
-      constexpr int ITEMS = 2 * 2 * M * NF;   // fam x s x k x f
-      for (int o = node; o < ITEMS; o += NPC) {
-        const int f = o % NF;
-        const int k = (o / NF) % M;
-        const int s = (o / (NF * M)) & 1;
-        const int fam = o / (2 * NF * M);
-        const int hi = f / st, lo = f - hi * st;
-        const double* src = St + ((fam == 0 ? 0 : (1 + a) * M) + k) * NPC + hi * st * N + lo;
-        const double* tv = s ? sTR : sTL;
-        double v = 0.0;
+    for (int k = 0; k < M; ++k) {
+      const double* sq = St + k * NPC + base;
+      const double* sf = St + ((1 + a) * M + k) * NPC + base;
+      double q0 = 0.0, q1 = 0.0, f0 = 0.0, f1 = 0.0;
 #pragma unroll
-        for (int j = 0; j < N; ++j) v = fma(tv[j], src[j * st], v);
-        (fam == 0 ? A.trace_q : A.trace_f)[tbase + ((2 * a + s) * M + k) * NF + f] = v;
+      for (int j = 0; j < N; ++j) {
+        const double vq = sq[j * st], vf = sf[j * st];
+        q0 = fma(sTL[j], vq, q0);
+        q1 = fma(sTR[j], vq, q1);
+        f0 = fma(sTL[j], vf, f0);
+        f1 = fma(sTR[j], vf, f1);
       }
+      const size_t o0 = tbase + ((size_t)(2 * a) * M + k) * NF + f;
+      const size_t o1 = tbase + ((size_t)(2 * a + 1) * M + k) * NF + f;
+      A.trace_q[o0] = q0;
+      A.trace_q[o1] = q1;
+      A.trace_f[o0] = f0;
+      A.trace_f[o1] = f1;
     }
   }
   if (A.iter_total) {
