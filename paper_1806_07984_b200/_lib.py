@@ -14,7 +14,8 @@ import re
 from .errors import STATUS_ERRORS, NativeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libenclavedg_b200.so")
+# EDG_LIB overrides the path (A/B variants built by build_lib --variant)
+LIB_PATH = os.environ.get("EDG_LIB") or os.path.join(HERE, "_lib", "libenclavedg_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "enclavedg_b200.h")
 
 PDE_KIND = {"advection": 0, "burgers": 1, "euler": 2}

@@ -33,8 +33,8 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, obj):
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+def _compile(src, obj, defines=()):
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     log = obj + ".ptxas.txt"
     with open(log, "w") as fh:
@@ -44,34 +44,40 @@ def _compile(src, obj):
     return obj
 
 
-def build(jobs=None, force=False, verbose=True):
-    os.makedirs(OUT_DIR, exist_ok=True)
+def build(jobs=None, force=False, verbose=True, defines=(), variant=None):
+    """Build the library; `defines` (e.g. EDG_FV_CPT=1) with a `variant` name
+    go to _lib/<variant>/ for A/B experiments (load with EDG_LIB=<path>)."""
+    out_dir = OUT_DIR if variant is None else os.path.join(OUT_DIR, variant)
+    lib = os.path.join(out_dir, "libenclavedg_b200.so")
+    os.makedirs(out_dir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(os.path.dirname(HERE), "include", "*.h"))
     objs = []
     todo = []
     for s in srcs:
-        o = os.path.join(OUT_DIR, os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(out_dir, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _stale(o, [s, *hdrs]):
             todo.append((s, o))
     if todo:
         jobs = jobs or min(len(todo), os.cpu_count() or 4)
         with cf.ThreadPoolExecutor(jobs) as ex:
-            list(ex.map(lambda so: _compile(*so), todo))
+            list(ex.map(lambda so: _compile(*so, defines=defines), todo))
         if verbose:
             print(f"compiled {len(todo)} unit(s)", file=sys.stderr)
-    if force or todo or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    if force or todo or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stderr[-4000:]}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--jobs", type=int, default=None)
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--variant", default=None)
     a = ap.parse_args()
-    print(build(a.jobs, a.force))
+    print(build(a.jobs, a.force, defines=a.defines, variant=a.variant))

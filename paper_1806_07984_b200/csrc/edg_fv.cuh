@@ -47,9 +47,12 @@ struct FvCfg {
   static constexpr int KEZ = (KE % 2) ? KE : KE + 1;    // last axis padded to an odd length
   static constexpr int NE = ipow(KE, DIM - 1) * KEZ;    // (bank-conflict-free strided access)
   static constexpr int NL = ipow(K, DIM - 1);           // cells per face layer
-  static constexpr int CPT = (K % 2 == 0 && NC >= 256) ? 2 : 1;   // volumes per thread (pairs along the last axis)
+#ifndef EDG_FV_CPT
+#define EDG_FV_CPT 2
+#endif
+  static constexpr int CPT = (K % 2 == 0 && NC >= 256) ? EDG_FV_CPT : 1;   // volumes per thread (pairs along the last axis)
   static constexpr int THREADS = ((NC / CPT + 31) / 32) * 32;
-  static constexpr int MINB = THREADS <= 256 ? 3 : 1;
+  static constexpr int MINB = THREADS <= 256 ? 3 : 2;
 };
 
 template <int KIND, int DIM, int K>
