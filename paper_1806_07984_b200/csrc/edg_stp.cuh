@@ -11,9 +11,9 @@
 // Per Picard iteration and cell, with B[r][s] = K^-1[r][s] * (-dt w_s) and
 // c = K^-1 lift (kernels.py:134-142):
 //     acc[r] = c_r q + sum_s B[r][s] sum_a (D/h_a) (x)_a F_a(qhat_s)
-// then delta = max |acc - qhat| over the cell (NaN-propagating, via 64-bit
-// atomicMax on bit patterns) decides the per-cell exit exactly like
-// kernels.py:143-147 (delta < tol).  Converged cells stop updating; the CTA
+// then the per-cell exit of kernels.py:143-147 (delta = max |acc - qhat| <
+// tol, NaN never below) is decided as "every |acc - qhat| < tol" by a
+// per-thread predicate and a per-cell shared flag.  Converged cells stop updating; the CTA
 // runs until its last cell stops (the solver orders cells by their previous
 // Picard count so that CTAs are homogeneous).  The epilogue
 // (kernels.py:148-157) forms q_end, q_int and the time-integrated flux,
@@ -83,7 +83,11 @@ struct StpCfg {
   static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32;
   // resident CTAs per SM requested from ptxas (caps registers per thread)
   // (measured: 2 for the 2-D p=5 kernel, 3 for the 3-D p=4 kernel)
+#ifdef EDG_STP_MINB_2D
+  static constexpr int MINB = DIM == 2 ? EDG_STP_MINB_2D : 3;
+#else
   static constexpr int MINB = DIM == 2 ? 2 : 3;
+#endif
 };
 
 template <int KIND, int DIM, int N>
@@ -102,7 +106,7 @@ struct StpSmem {
 #else
   static constexpr int G = DIM == 2 ? 2 : 1;
 #endif
-  static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * G * FB) + sizeof(unsigned long long) * 2 * C::CPB;
+  static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * G * FB + C::CPB * M * C::NPC) + sizeof(int) * 2 * C::CPB;
 };
 
 template <int KIND, int DIM, int N, int MINB = StpCfg<DIM, N>::MINB>
@@ -129,7 +133,8 @@ stp_picard_kernel(const StpArgs A) {
   double* sBs = sC + N;              // sum_s B[r][s]
   double* sF = smem + Sm::OPS;       // flux buffers [2][CPB][DIM][M][NPCP], 16-byte aligned (OPS even)
   static_assert(Sm::OPS % 2 == 0 && Sm::OPS >= 2 * N * N + 5 * N, "operator block must keep sF 16-byte aligned");
-  unsigned long long* sRed = reinterpret_cast<unsigned long long*>(sF + 2 * Sm::G * Sm::FB);   // [2][CPB]
+  double* sQ0 = sF + 2 * Sm::G * Sm::FB;                       // initial state [CPB][M][NPC] (thread-private)
+  int* sFlag = reinterpret_cast<int*>(sQ0 + CPB * M * NPC);    // [2][CPB] "not converged" flags
 
   const int tid = threadIdx.x;
   int slot, node;
@@ -168,7 +173,7 @@ stp_picard_kernel(const StpArgs A) {
     for (int s = 0; s < N; ++s) bs += A.basis[EDG_BASIS_KINV(N) + i * N + s] * (-dt * A.basis[EDG_BASIS_W(N) + s]);
     sBs[i] = bs;
   }
-  for (int i = tid; i < 2 * CPB; i += THREADS) sRed[i] = 0ull;
+  for (int i = tid; i < 2 * CPB; i += THREADS) sFlag[i] = 0;
   __syncthreads();
 
   int ix[DIM];
@@ -199,10 +204,14 @@ stp_picard_kernel(const StpArgs A) {
   }
 
   const double* qsrc = A.q + (size_t)cell * M * NPC + node;
+  // the initial state is re-read every iteration (c_r q): keep a private copy
+  // in shared memory instead of re-fetching it through L1/L2
+  double* const q0s = sQ0 + slot * M * NPC + node;
   double qh[N][M], acc[N][M];
 #pragma unroll
   for (int k = 0; k < M; ++k) {
     const double v = has_cell ? __ldg(qsrc + k * NPC) : 1.0;
+    if (lane_ok) q0s[k * NPC] = v;
 #pragma unroll
     for (int r = 0; r < N; ++r) qh[r][k] = v;
   }
@@ -288,7 +297,7 @@ stp_picard_kernel(const StpArgs A) {
       if (active) {
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          const double q0 = __ldg(qsrc + k * NPC);    // L1-resident initial state
+          const double q0 = q0s[k * NPC];
 #pragma unroll
           for (int r = 0; r < N; ++r) acc[r][k] = sC[r] * q0;
         }
@@ -324,29 +333,31 @@ stp_picard_kernel(const StpArgs A) {
         __syncthreads();
       }
     }
-    unsigned long long* red = sRed + (it & 1) * CPB;
-    unsigned long long mk = 0ull;
+    // delta = max |acc - qhat| < tol  <=>  every |acc - qhat| < tol (a NaN
+    // fails the comparison exactly as it poisons np.max): a per-thread
+    // predicate (DADD + DSETP.AND per value) and a per-cell "some lane is not
+    // below tol" flag replace the max reduction
+    int* flag = sFlag + (it & 1) * CPB;
+    bool below = true;
     if (active) {
 #pragma unroll
       for (int r = 0; r < N; ++r)
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          const unsigned long long key = maxkey(fabs(acc[r][k] - qh[r][k]));
-          mk = key > mk ? key : mk;
+          below = below & (fabs(acc[r][k] - qh[r][k]) < A.tol);
           qh[r][k] = acc[r][k];
         }
+      if (!below) flag[slot] = 1;
     }
-    seg_max_atomic(red, lane_ok ? slot : -1, mk);
     __syncthreads();
     if (active) {
       its = it;
-      const double delta = from_maxkey(red[slot]);
-      if (delta < A.tol) {
+      if (flag[slot] == 0) {
         active = false;
         conv = true;
       }
     }
-    if (tid < CPB) sRed[((it + 1) & 1) * CPB + tid] = 0ull;
+    if (tid < CPB) sFlag[((it + 1) & 1) * CPB + tid] = 0;
     if (!__syncthreads_or(active)) break;
   }
 
