@@ -204,6 +204,44 @@ __device__ __forceinline__ void seg_max_atomic(unsigned long long* base, int seg
   if (seg >= 0 && key != 0ull && (lane == 0 || prev != seg)) atomicMax(base + seg, key);
 }
 
+// Same contract as seg_max_atomic, but the caller passes the lane mask of its
+// segment (lanes of this warp with the same `seg`): two 32-bit redux.sync
+// (high word, then low word among the lanes holding the high maximum) replace
+// the 5-step segmented shuffle; one shared-memory atomicMax per segment.
+__device__ __forceinline__ void seg_max_redux(unsigned long long* base, int seg, unsigned mask,
+                                              unsigned long long key) {
+  const unsigned hi = (unsigned)(key >> 32);
+  const unsigned mhi = __reduce_max_sync(mask, hi);
+  const unsigned mlo = __reduce_max_sync(mask, hi == mhi ? (unsigned)key : 0u);
+  const unsigned long long m = ((unsigned long long)mhi << 32) | mlo;
+  if (seg >= 0 && m != 0ull && (int)(threadIdx.x & 31) == __ffs(mask) - 1) atomicMax(base + seg, m);
+}
+
+// lane mask of the lanes of this warp whose thread index lies in [lo, hi)
+__device__ __forceinline__ unsigned lane_range_mask(int lo, int hi) {
+  const int wb = threadIdx.x & ~31;
+  const int s0 = max(lo, wb) - wb, s1 = min(hi, wb + 32) - wb;
+  if (s1 <= s0) return 1u << (threadIdx.x & 31);
+  const unsigned up = s1 >= 32 ? 0xffffffffu : ((1u << s1) - 1u);
+  return up & ~((1u << s0) - 1u);
+}
+
+// Division by a runtime divisor d >= 1 via multiply-high (x < 2^31).
+struct FastDiv {
+  unsigned d, m, l;
+  __device__ __forceinline__ void init(unsigned dd) {
+    d = dd;
+    l = 0;
+    while ((1u << l) < d) ++l;
+    m = l == 0 ? 0u : (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1ull);
+  }
+  __device__ __forceinline__ unsigned div(unsigned x) const {
+    if (l == 0) return x;
+    const unsigned t = __umulhi(x, m);
+    return (t + ((x - t) >> 1)) >> (l - 1);
+  }
+};
+
 // Python-max over axes of the per-axis node maxima (kernels.py:271-273):
 // lam = max(lam, ax) takes ax only if ax > lam, so a NaN axis is dropped.
 __device__ __forceinline__ double python_max(double lam, double ax) { return (ax > lam) ? ax : lam; }
@@ -212,6 +250,18 @@ __device__ __forceinline__ double python_max(double lam, double ax) { return (ax
 __device__ __forceinline__ double dt_candidate(double h, int order, double lam) {
   return __ddiv_rn(h, __dmul_rn((double)(2 * order + 1), lam));
 }
+
+// cp.async (LDGSTS) global -> shared copies and group completion
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 inline int check_launch() {
   cudaError_t e = cudaGetLastError();

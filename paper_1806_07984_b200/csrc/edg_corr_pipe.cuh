@@ -1,0 +1,232 @@
+// Pipelined corrector for uniform Cartesian meshes (edg_corrector_grid) --
+// the same computation and bits as corrector_kernel<..., FUSED = true> in
+// edg_faces.cuh (kernels.py:162-193 + the admissible-dt candidate of
+// kernels.py:267-281), restructured for HBM streaming:
+//
+//  * persistent CTAs (grid = SMs x resident CTAs) walk groups of CPB
+//    consecutive cells;
+//  * the next group's q_end block, own trace_q / trace_f blocks and the 2d
+//    neighbour face traces are copied global -> shared with cp.async
+//    (LDGSTS, 16-byte where aligned) while the current group is corrected
+//    out of shared memory (two stages), so every SM always has a group's
+//    bytes in flight instead of stalling each CTA on its own loads;
+//  * the admissible-dt candidate and the non-finite count are reduced per
+//    CTA across all its groups: one global atomic each per CTA.
+#pragma once
+#include "edg_faces.cuh"
+
+namespace edg {
+
+template <int KIND, int DIM, int N>
+struct CorrPipe {
+  using Cf = CorrCfg<DIM, N>;
+  static constexpr int M = Pde<KIND, DIM>::M;
+  static constexpr int NPC = Cf::NPC, NF = Cf::NF, CPB = Cf::CPB, THREADS = Cf::THREADS;
+  static constexpr int TRC = 2 * DIM * M * NF;            // trace doubles per cell (one family)
+  static constexpr int QE = (CPB * M * NPC + 1) & ~1;     // stage sub-blocks, even -> 16-byte aligned
+  static constexpr int TB = (CPB * TRC + 1) & ~1;
+  static constexpr int STAGE = QE + 3 * TB;               // q_end, trace_q, trace_f, neighbour trace_q
+  static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TB + 2 * DIM * N) +
+                                  sizeof(unsigned long long) * (DIM * CPB + CPB);
+};
+
+// contiguous block of n doubles, all threads of the CTA cooperating
+template <int THREADS>
+__device__ __forceinline__ void cp_block(double* dst, const double* src, int n, int tid) {
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const int n2 = n >> 1;
+    for (int i = tid; i < n2; i += THREADS) cp_async16(dst + 2 * i, src + 2 * i);
+    if ((n & 1) && tid == 0) cp_async8(dst + n - 1, src + n - 1);
+  } else {
+    for (int i = tid; i < n; i += THREADS) cp_async8(dst + i, src + i);
+  }
+}
+
+template <int KIND, int DIM, int N>
+__global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_kernel(const CorrArgs A) {
+  using P = Pde<KIND, DIM>;
+  using C = CorrPipe<KIND, DIM, N>;
+  constexpr int M = C::M, NPC = C::NPC, NF = C::NF, CPB = C::CPB, THREADS = C::THREADS, TRC = C::TRC;
+  constexpr int FPC = 2 * DIM * M * NF;     // neighbour doubles per cell (= TRC)
+  constexpr int TOT = 2 * DIM * NF;         // face points per cell
+
+  extern __shared__ __align__(16) double smem[];
+  double* const sStage = smem;                          // [2][STAGE]
+  double* const sJump = smem + 2 * C::STAGE;            // [CPB][2d][M][NF]
+  double* const sV = sJump + C::TB;                     // [2d][N] lift vectors (uniform cells)
+  unsigned long long* const sLam = reinterpret_cast<unsigned long long*>(sV + 2 * DIM * N);   // [DIM][CPB]
+  unsigned long long* const sFlag = sLam + DIM * CPB;   // [CPB] non-finite flags
+
+  const int tid = threadIdx.x;
+  const int slot = tid / NPC;
+  const int node = tid - slot * NPC;
+  const int n = A.grid_n;
+  const int ngroups = (A.ncells + CPB - 1) / CPB;
+
+  for (int i = tid; i < 2 * DIM * N; i += THREADS) {
+    const int fs = i / N, j = i % N;
+    const int a = fs >> 1, s = fs & 1;
+    const double tr = A.basis[(s ? EDG_BASIS_TR(N) : EDG_BASIS_TL(N)) + j];
+    const double sg = s ? 1.0 : -1.0;
+    sV[i] = __ddiv_rn(__dmul_rn(sg, tr), __dmul_rn(A.basis[EDG_BASIS_W(N) + j], A.edges[a]));
+  }
+  for (int i = tid; i < DIM * CPB; i += THREADS) sLam[i] = 0ull;
+  for (int i = tid; i < CPB; i += THREADS) sFlag[i] = 0ull;
+
+  // per-thread constants: node coordinates, face point of the node on each
+  // axis, and the lane mask of this thread's cell segment
+  int ix[DIM], fpt[DIM];
+  {
+    int t = node;
+#pragma unroll
+    for (int a = DIM - 1; a >= 0; --a) {
+      ix[a] = t % N;
+      t /= N;
+    }
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const int st = ipow(N, DIM - 1 - a);
+      fpt[a] = (node / (st * N)) * st + (node % st);
+    }
+  }
+  const unsigned segmask = lane_range_mask(slot * NPC, (slot + 1) * NPC);
+  FastDiv fdn, fdn2;
+  fdn.init((unsigned)n);
+  fdn2.init((unsigned)n * (unsigned)(DIM == 3 ? n : 1));
+
+  // issue the copies of group g into stage buffer st; the neighbour face
+  // blocks (M * NF contiguous doubles each) go one warp per block
+  auto load_group = [&](int g, double* st) {
+    const int c0 = g * CPB;
+    const int nc = min(CPB, A.ncells - c0);
+    cp_block<THREADS>(st, A.q_end + (size_t)c0 * M * NPC, nc * M * NPC, tid);
+    cp_block<THREADS>(st + C::QE, A.trace_q + (size_t)c0 * TRC, nc * TRC, tid);
+    cp_block<THREADS>(st + C::QE + C::TB, A.trace_f + (size_t)c0 * TRC, nc * TRC, tid);
+    double* nq = st + C::QE + 2 * C::TB;
+    constexpr int BLK = M * NF;
+    constexpr int NW = THREADS / 32;
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int bi = warp; bi < nc * 2 * DIM; bi += NW) {
+      const int sl = bi / (2 * DIM), fs = bi - sl * (2 * DIM);
+      const int a = fs >> 1, s = fs & 1;
+      const unsigned cell = (unsigned)(c0 + sl);
+      const unsigned q = a == DIM - 1 ? cell : (a == DIM - 2 ? fdn.div(cell) : fdn2.div(cell));
+      const int ia = (int)(q - fdn.div(q) * (unsigned)n);
+      const int stride = a == DIM - 1 ? 1 : (a == DIM - 2 ? n : n * n);
+      int j = ia + (s ? 1 : -1);
+      if (j < 0 || j >= n) j = A.periodic ? (j < 0 ? n - 1 : 0) : -1;
+      // neighbour's opposite face, or (outflow) the cell's own trace
+      const double* src = j >= 0 ? A.trace_q + (size_t)((int)cell + (j - ia) * stride) * TRC + (size_t)(2 * a + (1 - s)) * BLK
+                                 : A.trace_q + (size_t)cell * TRC + (size_t)fs * BLK;
+      double* dst = nq + (sl * 2 * DIM + fs) * BLK;
+      if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        for (int i = lane; i < BLK / 2; i += 32) cp_async16(dst + 2 * i, src + 2 * i);
+        if ((BLK & 1) && lane == 0) cp_async8(dst + BLK - 1, src + BLK - 1);
+      } else {
+        for (int i = lane; i < BLK; i += 32) cp_async8(dst + i, src + i);
+      }
+    }
+  };
+
+  unsigned long long best = DT_EMPTY;   // per-CTA dt candidate (threads < CPB)
+  unsigned int nonfinite = 0u;
+
+  int g = blockIdx.x;
+  if (g < ngroups) load_group(g, sStage);
+  cp_async_commit();
+  for (int it = 0; g < ngroups; g += gridDim.x, ++it) {
+    double* const cur = sStage + (it & 1) * C::STAGE;
+    const int gn = g + gridDim.x;
+    if (gn < ngroups) load_group(gn, sStage + ((it + 1) & 1) * C::STAGE);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+
+    const int cell = g * CPB + slot;
+    const bool has_cell = slot < CPB && cell < A.ncells;
+    const double* qe = cur;
+    const double* tq = cur + C::QE;
+    const double* tf = cur + C::QE + C::TB;
+    const double* nq = cur + C::QE + 2 * C::TB;
+    // phase 1: Rusanov outcome - trace_f on the 2d faces (corrector_kernel order)
+    if (has_cell) {
+      for (int f2 = node; f2 < TOT; f2 += NPC) {
+        const int fs = f2 / NF, f = f2 - fs * NF;
+        const int a = fs >> 1, s = fs & 1;
+        double mine[M], theirs[M], out[M];
+        const int b = slot * TRC + fs * M * NF + f;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          mine[k] = tq[b + k * NF];
+          theirs[k] = nq[b + k * NF];
+        }
+        if (s == 1)
+          rusanov<KIND, DIM>(mine, theirs, a, 1, A.pp, out);
+        else
+          rusanov<KIND, DIM>(theirs, mine, a, 1, A.pp, out);
+#pragma unroll
+        for (int k = 0; k < M; ++k) sJump[b + k * NF] = __dsub_rn(out[k], tf[b + k * NF]);
+      }
+    }
+    __syncthreads();
+    // phase 2: Q = q_end - sum v (x) jump in the reference (a, s) order
+    double qn[M];
+    bool finite = true;
+#pragma unroll
+    for (int k = 0; k < M; ++k) qn[k] = has_cell ? qe[(slot * M + k) * NPC + node] : 0.0;
+    if (has_cell) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const double v = sV[(2 * a + s) * N + ix[a]];
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            qn[k] = __dsub_rn(qn[k], __dmul_rn(v, sJump[slot * TRC + ((2 * a + s) * M + k) * NF + fpt[a]]));
+        }
+      }
+      double* qo = A.q_out + (size_t)cell * M * NPC + node;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        qo[(size_t)k * NPC] = qn[k];
+        finite = finite && (fabs(qn[k]) <= 1.7976931348623157e308);
+      }
+    }
+    if (A.dt_slots) {
+      unsigned long long lk[DIM];
+      const auto pr = P::parts(qn, A.pp);
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) lk[a] = has_cell ? maxkey(P::lam(qn, pr, a, A.pp)) : 0ull;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) seg_max_redux(sLam + a * CPB, has_cell ? slot : -1, segmask, lk[a]);
+    }
+    if (has_cell && !finite) sFlag[slot] = 1ull;
+    __syncthreads();
+    if (tid < CPB) {
+      const int c = g * CPB + tid;
+      if (c < A.ncells) {
+        if (sFlag[tid]) ++nonfinite;
+        if (A.dt_slots) {
+          double lam = 0.0;
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) lam = python_max(lam, from_maxkey(sLam[a * CPB + tid]));
+          if (lam > 0.0) {
+            const unsigned long long cand =
+                (unsigned long long)__double_as_longlong(dt_candidate(A.hmin[0], A.order, lam));
+            best = cand < best ? cand : best;
+          }
+        }
+      }
+      sFlag[tid] = 0ull;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) sLam[a * CPB + tid] = 0ull;
+    }
+  }
+  cp_async_wait1();   // (only empty groups can be outstanding here)
+  if (tid < CPB) {
+    if (A.status && nonfinite) atomicAdd(A.status + 1, nonfinite);
+    if (A.dt_slots && best != DT_EMPTY) atomicMin(A.dt_slots + (blockIdx.x * CPB + tid) % EDG_DT_SLOTS, best);
+  }
+}
+
+}  // namespace edg

@@ -201,8 +201,9 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
     const auto pr = P::parts(qn, A.pp);
 #pragma unroll
     for (int a = 0; a < DIM; ++a) lk[a] = has_cell ? maxkey(P::lam(qn, pr, a, A.pp)) : 0ull;
+    const unsigned segmask = lane_range_mask(slot * NPC, (slot + 1) * NPC);
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) seg_max_atomic(sLam + a * CPB, has_cell ? slot : -1, lk[a]);
+    for (int a = 0; a < DIM; ++a) seg_max_redux(sLam + a * CPB, has_cell ? slot : -1, segmask, lk[a]);
   }
   // per-cell non-finite flag (counted once per cell)
   if (has_cell && !finite) atomicOr(reinterpret_cast<unsigned int*>(sBest + slot), 1u);

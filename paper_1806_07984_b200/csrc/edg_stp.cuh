@@ -106,7 +106,15 @@ struct StpSmem {
 #else
   static constexpr int G = DIM == 2 ? 2 : 1;
 #endif
-  static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * G * FB + C::CPB * M * C::NPC) + sizeof(int) * 2 * C::CPB;
+  // EDG_STP_QHS: keep the Picard iterate qhat in (thread-private) shared
+  // memory instead of registers (fewer registers, more resident CTAs)
+#ifdef EDG_STP_QHS
+  static constexpr bool QHS = true;
+#else
+  static constexpr bool QHS = false;
+#endif
+  static constexpr int QH = QHS ? C::CPB * N * M * C::NPC : 0;
+  static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * G * FB + 2 * C::CPB * M * C::NPC + QH) + sizeof(int) * 2 * C::CPB;
 };
 
 template <int KIND, int DIM, int N, int MINB = StpCfg<DIM, N>::MINB>
@@ -133,8 +141,9 @@ stp_picard_kernel(const StpArgs A) {
   double* sBs = sC + N;              // sum_s B[r][s]
   double* sF = smem + Sm::OPS;       // flux buffers [2][CPB][DIM][M][NPCP], 16-byte aligned (OPS even)
   static_assert(Sm::OPS % 2 == 0 && Sm::OPS >= 2 * N * N + 5 * N, "operator block must keep sF 16-byte aligned");
-  double* sQ0 = sF + 2 * Sm::G * Sm::FB;                       // initial state [CPB][M][NPC] (thread-private)
-  int* sFlag = reinterpret_cast<int*>(sQ0 + CPB * M * NPC);    // [2][CPB] "not converged" flags
+  double* sQ0 = sF + 2 * Sm::G * Sm::FB;                       // initial state [2][CPB][M][NPC] (thread-private)
+  double* sQH = sQ0 + 2 * CPB * M * NPC;                      // qhat [CPB][N][M][NPC] when Sm::QHS
+  int* sFlag = reinterpret_cast<int*>(sQH + Sm::QH);          // [2][CPB] "not converged" flags
 
   const int tid = threadIdx.x;
   int slot, node;
@@ -153,10 +162,26 @@ stp_picard_kernel(const StpArgs A) {
     node = tid - slot * NPC;
     lane_ok = slot < CPB;
   }
-  const int item = blockIdx.x * CPB + slot;
-  const bool has_cell = lane_ok && (item < A.nwork);
-  const int cell = has_cell ? (A.cell_list ? __ldg(A.cell_list + item) : item) : 0;
   const double dt = *A.dt;
+  // persistent CTAs: work blocks blockIdx.x, blockIdx.x + gridDim.x, ...; the
+  // next block's initial state is copied into the other staging buffer with
+  // cp.async while this one iterates (thread-private: each thread copies and
+  // later reads only its own node, so no barrier guards the buffers)
+  const int nblocks = (A.nwork + CPB - 1) / CPB;
+  constexpr int QB = CPB * M * NPC;
+  auto prefetch_q = [&](int b, int buf) {
+    const int itm = b * CPB + slot;
+    if (lane_ok && itm < A.nwork) {
+      const int c = A.cell_list ? __ldg(A.cell_list + itm) : itm;
+      const double* src = A.q + (size_t)c * M * NPC + node;
+      double* dst = sQ0 + buf * QB + slot * M * NPC + node;
+#pragma unroll
+      for (int k = 0; k < M; ++k) cp_async8(dst + k * NPC, src + k * NPC);
+    }
+  };
+  int blk = blockIdx.x;
+  if (blk < nblocks) prefetch_q(blk, 0);
+  cp_async_commit();
 
   for (int i = tid; i < N * N; i += THREADS) {
     sD[i] = A.basis[EDG_BASIS_D(N) + i];
@@ -173,7 +198,6 @@ stp_picard_kernel(const StpArgs A) {
     for (int s = 0; s < N; ++s) bs += A.basis[EDG_BASIS_KINV(N) + i * N + s] * (-dt * A.basis[EDG_BASIS_W(N) + s]);
     sBs[i] = bs;
   }
-  for (int i = tid; i < 2 * CPB; i += THREADS) sFlag[i] = 0;
   __syncthreads();
 
   int ix[DIM];
@@ -191,6 +215,15 @@ stp_picard_kernel(const StpArgs A) {
   int pb[DIM];
 #pragma unroll
   for (int a = 0; a < DIM; ++a) pb[a] = bnode - ix[a] * (a == DIM - 1 ? 1 : NP * ipow(N, DIM - 2 - a));
+  unsigned its_sum = 0u;
+
+  for (int gi = 0; blk < nblocks; blk += gridDim.x, ++gi) {
+  const int item = blk * CPB + slot;
+  const bool has_cell = lane_ok && (item < A.nwork);
+  const int cell = has_cell ? (A.cell_list ? __ldg(A.cell_list + item) : item) : 0;
+  if (blk + (int)gridDim.x < nblocks) prefetch_q(blk + gridDim.x, (gi + 1) & 1);
+  cp_async_commit();
+  if (tid < 2 * CPB) sFlag[tid] = 0;
   // derivative rows of this node, scaled by 1/h_a
   double Dr[DIM][N];
   {
@@ -202,18 +235,34 @@ stp_picard_kernel(const StpArgs A) {
       for (int j = 0; j < N; ++j) Dr[a][j] = sD[ix[a] * N + j] * ih;
     }
   }
+  cp_async_wait1();   // this block's initial state (own node) has landed
 
-  const double* qsrc = A.q + (size_t)cell * M * NPC + node;
-  // the initial state is re-read every iteration (c_r q): keep a private copy
-  // in shared memory instead of re-fetching it through L1/L2
-  double* const q0s = sQ0 + slot * M * NPC + node;
-  double qh[N][M], acc[N][M];
+  // the initial state is re-read every iteration (c_r q): private copy in
+  // shared memory
+  double* const q0s = sQ0 + (gi & 1) * QB + slot * M * NPC + node;
+  constexpr bool QHS = Sm::QHS;
+  double qhr[QHS ? 1 : N][M], acc[N][M];
+  double* const qhs = sQH + slot * N * M * NPC + node;
+  auto qget = [&](int r, int k) -> double {
+    if constexpr (QHS) return qhs[(r * M + k) * NPC];
+    else return qhr[r][k];
+  };
+  auto qset = [&](int r, int k, double v) {
+    if constexpr (QHS) {
+      if (lane_ok) qhs[(r * M + k) * NPC] = v;
+    } else {
+      qhr[r][k] = v;
+    }
+  };
+  auto qrow = [&](int r, double (&out)[M]) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) out[k] = qget(r, k);
+  };
 #pragma unroll
   for (int k = 0; k < M; ++k) {
-    const double v = has_cell ? __ldg(qsrc + k * NPC) : 1.0;
-    if (lane_ok) q0s[k * NPC] = v;
+    const double v = has_cell ? q0s[k * NPC] : 1.0;
 #pragma unroll
-    for (int r = 0; r < N; ++r) qh[r][k] = v;
+    for (int r = 0; r < N; ++r) qset(r, k, v);
   }
 
   bool active = has_cell;
@@ -279,7 +328,11 @@ stp_picard_kernel(const StpArgs A) {
       // qhat_s = q for every time node (kernels.py:134), so the first
       // iteration needs one flux and one derivative:
       //   acc[r] = c_r q + (sum_s B[r][s]) div F(q)
-      if (active) put_flux(buf0, qh[0]);
+      if (active) {
+        double q[M];
+        qrow(0, q);
+        put_flux(buf0, q);
+      }
       __syncthreads();
       if (active) {
         double dv[M];
@@ -287,7 +340,7 @@ stp_picard_kernel(const StpArgs A) {
 #pragma unroll
         for (int k = 0; k < M; ++k) {
 #pragma unroll
-          for (int r = 0; r < N; ++r) acc[r][k] = fma(sBs[r], dv[k], sC[r] * qh[r][k]);
+          for (int r = 0; r < N; ++r) acc[r][k] = fma(sBs[r], dv[k], sC[r] * qget(r, k));
         }
       }
     } else {
@@ -303,7 +356,11 @@ stp_picard_kernel(const StpArgs A) {
         }
 #pragma unroll
         for (int g = 0; g < G; ++g)
-          if (g < N) put_flux(slotbuf(0, g), qh[g]);
+          if (g < N) {
+            double q[M];
+            qrow(g, q);
+            put_flux(slotbuf(0, g), q);
+          }
       }
       __syncthreads();
       // software pipeline: the fluxes of the next G time nodes are evaluated
@@ -315,7 +372,11 @@ stp_picard_kernel(const StpArgs A) {
         if (active) {
 #pragma unroll
           for (int g = 0; g < G; ++g)
-            if (s0 + G + g < N) put_flux(slotbuf(stage ^ 1, g), qh[s0 + G + g]);
+            if (s0 + G + g < N) {
+              double q[M];
+              qrow(s0 + G + g, q);
+              put_flux(slotbuf(stage ^ 1, g), q);
+            }
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             if (s0 + g < N) {
@@ -344,8 +405,8 @@ stp_picard_kernel(const StpArgs A) {
       for (int r = 0; r < N; ++r)
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          below = below & (fabs(acc[r][k] - qh[r][k]) < A.tol);
-          qh[r][k] = acc[r][k];
+          below = below & (fabs(acc[r][k] - qget(r, k)) < A.tol);
+          qset(r, k, acc[r][k]);
         }
       if (!below) flag[slot] = 1;
     }
@@ -378,11 +439,13 @@ stp_picard_kernel(const StpArgs A) {
     for (int r = 0; r < N; ++r) {
       const double tr = sTR[r], w = sW[r];
       double F[DIM][M];
-      FastFlux<KIND, DIM>::template all<M>(qh[r], A.pp, F);
+      double q[M];
+      qrow(r, q);
+      FastFlux<KIND, DIM>::template all<M>(q, A.pp, F);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        qe[k] = fma(tr, qh[r][k], qe[k]);
-        qi[k] = fma(w, qh[r][k], qi[k]);
+        qe[k] = fma(tr, q[k], qe[k]);
+        qi[k] = fma(w, q[k], qi[k]);
       }
 #pragma unroll
       for (int a = 0; a < DIM; ++a)
@@ -445,12 +508,16 @@ stp_picard_kernel(const StpArgs A) {
       A.trace_f[o1] = f1;
     }
   }
+  if (has_cell && node == 0) its_sum += (unsigned)its;
+  // staging / flux buffers are reused by the next work block
+  __syncthreads();
+  }  // work blocks
   if (A.iter_total) {
     // per-CTA sum of iteration counts (algorithmic-flop accounting), one atomic per CTA
     __shared__ unsigned int sIts;
     if (tid == 0) sIts = 0u;
     __syncthreads();
-    if (has_cell && node == 0) atomicAdd(&sIts, (unsigned)its);
+    if (its_sum) atomicAdd(&sIts, its_sum);
     __syncthreads();
     if (tid == 0 && sIts) atomicAdd(A.iter_total, (unsigned long long)sIts);
   }
