@@ -59,7 +59,7 @@ template <int KIND, int DIM, int K>
 struct FvSmem {
   static constexpr int M = Pde<KIND, DIM>::M;
   static constexpr int NPARTS = KIND == EDG_PDE_EULER ? 3 : 0;
-  static constexpr size_t BYTES = sizeof(double) * FvCfg<DIM, K>::NE * (M + NPARTS) + sizeof(unsigned long long) * DIM;
+  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + DIM) + sizeof(unsigned long long) * DIM;
 };
 
 template <int KIND, int DIM, int K, int MINB = FvCfg<DIM, K>::MINB>
@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
   double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler)
   double* sC = sP + (EULER ? NE : 0);              // [NE] (Euler) sound speed
   unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sC + (EULER ? NE : 0));
+  double* sCoef = reinterpret_cast<double*>(sLam + DIM);   // [DIM] dt / (edge / K)
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
@@ -201,7 +202,8 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
 #pragma unroll
   for (int u = 0; u < NHT; ++u)
     if (xh_[u] >= 0) stage(xh_[u], qh_[u]);
-  const double dt = *A.dt;
+  // dt / dx_a, once per CTA (kernels.py:241: dt / (h / k) with exact divisions)
+  if (tid < DIM) sCoef[tid] = __ddiv_rn(*A.dt, __ddiv_rn(A.edges[tid], (double)K));
   __syncthreads();
 
   // ---- own volumes (CPT consecutive along the last axis) ----
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
   }
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
-    const double coef = __ddiv_rn(dt, __ddiv_rn(A.edges[a], (double)K));
+    const double coef = sCoef[a];
     const int st = estride(a);
     if (a == DIM - 1 && CPT == 2) {
       // interfaces (x0-1 | x0), (x0 | x0+1) shared, (x0+1 | x0+2)

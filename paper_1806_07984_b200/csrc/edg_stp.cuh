@@ -99,7 +99,22 @@ struct StpSmem {
   // pencil pairs along it are 16-byte aligned
   static constexpr int NP = N;   // (padding odd N to N+1 for pair loads measured slower on 3-D p=4)
   static constexpr int NPCP = C::NPC / N * NP;
-  static constexpr int FB = C::CPB * DIM * M * NPCP;            // one flux buffer
+  // EDG_STP_T0=1 (2-D, even N): store the axis-0 flux transposed ([k][j][i],
+  // pencils contiguous) so both derivative axes use 16-byte pair loads
+  // (measured 3% slower on cfg2 at CFL 0.9: off by default)
+#ifndef EDG_STP_T0
+#define EDG_STP_T0 0
+#endif
+  static constexpr bool T0 = EDG_STP_T0 && DIM == 2 && N % 2 == 0;
+  // EDG_STP_SPAD=1: per-cell flux block stride padded to 8 (mod 16) doubles
+  // so the same pencil of two cells sharing a warp lands 16 banks apart
+  // (removes the 2-way conflicts but measured no faster: off by default)
+#ifndef EDG_STP_SPAD
+#define EDG_STP_SPAD 0
+#endif
+  static constexpr int SS0 = DIM * M * NPCP;
+  static constexpr int SS = (EDG_STP_SPAD && C::CPB > 1) ? SS0 + ((8 - SS0 % 16) + 16) % 16 : SS0;
+  static constexpr int FB = C::CPB * SS;                        // one flux buffer
   // time nodes per pipeline stage (one barrier per stage); EDG_STP_G overrides
 #ifdef EDG_STP_G
   static constexpr int G = EDG_STP_G;
@@ -215,6 +230,9 @@ stp_picard_kernel(const StpArgs A) {
   int pb[DIM];
 #pragma unroll
   for (int a = 0; a < DIM; ++a) pb[a] = bnode - ix[a] * (a == DIM - 1 ? 1 : NP * ipow(N, DIM - 2 - a));
+  // transposed axis-0 layout: node (i, j) stored at j * N + i, pencil base j * N
+  const int tnode = DIM == 2 ? ix[DIM - 1] * N + ix[0] : 0;
+  if constexpr (Sm::T0) pb[0] = ix[DIM - 1] * N;
   unsigned its_sum = 0u;
 
   for (int gi = 0; blk < nblocks; blk += gridDim.x, ++gi) {
@@ -269,7 +287,7 @@ stp_picard_kernel(const StpArgs A) {
   int its = 0;
   bool conv = false;
   const int max_iter = A.max_iter;
-  double* const buf0 = sF + slot * (DIM * M * NPCP);
+  double* const buf0 = sF + slot * Sm::SS;
   double* const buf1 = buf0 + Sm::FB;
 
   // flux of one time node of this node's column -> flux buffer [a][k][node]
@@ -279,7 +297,7 @@ stp_picard_kernel(const StpArgs A) {
 #pragma unroll
     for (int a = 0; a < DIM; ++a)
 #pragma unroll
-      for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPCP + bnode] = F[a][k];
+      for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPCP + ((Sm::T0 && a == 0) ? tnode : bnode)] = F[a][k];
   };
   // dv[k] = sum_a sum_j (D/h_a)[i_a][j] F_a[k][pencil_a(j)]
   auto deriv = [&](const double* Fb, double (&dv)[M]) {
@@ -294,7 +312,7 @@ stp_picard_kernel(const StpArgs A) {
       for (int k = 0; k < M; ++k) {
         const double* Fa = Fb + (a * M + k) * NPCP + pb[a];
         double acc_ak = (SPLIT || a == 0) ? 0.0 : part[a > 0 ? a - 1 : 0][k];
-        if (a == DIM - 1 && (N % 2 == 0)) {
+        if ((a == DIM - 1 || (Sm::T0 && a == 0)) && (N % 2 == 0)) {
           // contiguous pencil: 16-byte pair loads (lanes of one pencil broadcast)
 #pragma unroll
           for (int j = 0; j + 1 < N; j += 2) {

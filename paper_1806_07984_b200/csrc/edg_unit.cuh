@@ -6,6 +6,7 @@
 
 #include "edg_stp.cuh"
 #include "edg_stp_th.cuh"
+#include "edg_stp_pen.cuh"
 #include "edg_stp_ck.cuh"
 #include "edg_faces.cuh"
 #include "edg_corr_pipe.cuh"
@@ -71,6 +72,28 @@ static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
       if (set_smem(kern, smem)) return EDG_ERR_CUDA;
       const int blocks = (a.nwork + Ct::CPB - 1) / Ct::CPB;
       if (blocks > 0) kern<<<blocks, Ct::THREADS, smem, st>>>(a);
+      return check_launch();
+    }
+  }
+  if constexpr (DIM == 2 && N <= 6) {
+    // pencil formulation (edg_stp_pen.cuh): EDG_STP_PEN=1 selects it
+    static const int pen = [] {
+      const char* v = getenv("EDG_STP_PEN");
+      return v ? atoi(v) : 0;
+    }();
+    if (pen) {
+      using Cp = PenCfg<KIND, N>;
+      auto kern = stp_pencil_kernel<KIND, N>;
+      if (set_smem(kern, Cp::BYTES)) return EDG_ERR_CUDA;
+      // operator table head -> this unit's constant bank (device to device, in stream order)
+      if (cudaMemcpyToSymbolAsync(kPen, a.basis, sizeof(double) * pen_ops(N), sizeof(double) * pen_off(N),
+                                  cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return EDG_ERR_CUDA;
+      const int blocks = (a.nwork + Cp::CPB - 1) / Cp::CPB;
+      const int cap = persistent_grid(kern, Cp::THREADS, Cp::BYTES);
+      if (cap < 0) return EDG_ERR_CUDA;
+      const int grid = blocks < cap ? blocks : cap;
+      if (grid > 0) kern<<<grid, Cp::THREADS, Cp::BYTES, st>>>(a);
       return check_launch();
     }
   }
