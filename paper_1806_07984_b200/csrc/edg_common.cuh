@@ -39,6 +39,10 @@ struct Pde<EDG_PDE_ADVECTION, DIM> {
   __device__ __forceinline__ static double lam(const double*, const Parts&, int a, const PdeParams& pp) {
     return fabs(pp.vel[a]);
   }
+  __device__ __forceinline__ static void lam_all(const double* q, const Parts& pr, const PdeParams& pp, double* l) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) l[a] = lam(q, pr, a, pp);
+  }
 };
 
 // pde.py:40-49: F = 0.5 * q * q (every axis), lambda = |q|
@@ -53,6 +57,10 @@ struct Pde<EDG_PDE_BURGERS, DIM> {
   }
   __device__ __forceinline__ static double lam(const double* q, const Parts&, int, const PdeParams&) {
     return fabs(q[0]);
+  }
+  __device__ __forceinline__ static void lam_all(const double* q, const Parts& pr, const PdeParams& pp, double* l) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) l[a] = lam(q, pr, a, pp);
   }
 };
 
@@ -98,6 +106,12 @@ struct Pde<EDG_PDE_EULER, DIM> {
     const double u = __dmul_rn(mom(q, a), pr.inv);
     const double c = __dsqrt_rn(__dmul_rn(__dmul_rn(pp.gamma, pr.p), pr.inv));
     return __dadd_rn(fabs(u), c);
+  }
+  // every axis at once: the sound speed (one sqrt) is shared, same operations
+  __device__ __forceinline__ static void lam_all(const double* q, const Parts& pr, const PdeParams& pp, double* l) {
+    const double c = __dsqrt_rn(__dmul_rn(__dmul_rn(pp.gamma, pr.p), pr.inv));
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) l[a] = __dadd_rn(fabs(__dmul_rn(q[1 + a], pr.inv)), c);
   }
 };
 
@@ -262,6 +276,18 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// contiguous block of n doubles, all threads of the CTA cooperating
+template <int THREADS>
+__device__ __forceinline__ void cp_block(double* dst, const double* src, int n, int tid) {
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const int n2 = n >> 1;
+    for (int i = tid; i < n2; i += THREADS) cp_async16(dst + 2 * i, src + 2 * i);
+    if ((n & 1) && tid == 0) cp_async8(dst + n - 1, src + n - 1);
+  } else {
+    for (int i = tid; i < n; i += THREADS) cp_async8(dst + i, src + i);
+  }
+}
 
 inline int check_launch() {
   cudaError_t e = cudaGetLastError();

@@ -30,18 +30,6 @@ struct CorrPipe {
                                   sizeof(unsigned long long) * (DIM * CPB + CPB);
 };
 
-// contiguous block of n doubles, all threads of the CTA cooperating
-template <int THREADS>
-__device__ __forceinline__ void cp_block(double* dst, const double* src, int n, int tid) {
-  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-    const int n2 = n >> 1;
-    for (int i = tid; i < n2; i += THREADS) cp_async16(dst + 2 * i, src + 2 * i);
-    if ((n & 1) && tid == 0) cp_async8(dst + n - 1, src + n - 1);
-  } else {
-    for (int i = tid; i < n; i += THREADS) cp_async8(dst + i, src + i);
-  }
-}
-
 template <int KIND, int DIM, int N>
 __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_kernel(const CorrArgs A) {
   using P = Pde<KIND, DIM>;
@@ -196,7 +184,13 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
       unsigned long long lk[DIM];
       const auto pr = P::parts(qn, A.pp);
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) lk[a] = has_cell ? maxkey(P::lam(qn, pr, a, A.pp)) : 0ull;
+      for (int a = 0; a < DIM; ++a) lk[a] = 0ull;
+      if (has_cell) {
+        double l[DIM];
+        P::lam_all(qn, pr, A.pp, l);
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) lk[a] = maxkey(l[a]);
+      }
 #pragma unroll
       for (int a = 0; a < DIM; ++a) seg_max_redux(sLam + a * CPB, has_cell ? slot : -1, segmask, lk[a]);
     }

@@ -34,9 +34,11 @@ __global__ void __launch_bounds__(256) cell_speed_kernel(int ncells, int npts, c
 #pragma unroll
       for (int k = 0; k < M; ++k) s[k] = qc[(size_t)k * npts + i];
       const auto pr = P::parts(s, pp);
+      double l[DIM];
+      P::lam_all(s, pr, pp, l);
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
-        const unsigned long long kk = maxkey(P::lam(s, pr, a, pp));
+        const unsigned long long kk = maxkey(l[a]);
         key[a] = kk > key[a] ? kk : key[a];
       }
     }

@@ -200,7 +200,13 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
     unsigned long long lk[DIM];
     const auto pr = P::parts(qn, A.pp);
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) lk[a] = has_cell ? maxkey(P::lam(qn, pr, a, A.pp)) : 0ull;
+    for (int a = 0; a < DIM; ++a) lk[a] = 0ull;
+    if (has_cell) {
+      double l[DIM];
+      P::lam_all(qn, pr, A.pp, l);
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) lk[a] = maxkey(l[a]);
+    }
     const unsigned segmask = lane_range_mask(slot * NPC, (slot + 1) * NPC);
 #pragma unroll
     for (int a = 0; a < DIM; ++a) seg_max_redux(sLam + a * CPB, has_cell ? slot : -1, segmask, lk[a]);

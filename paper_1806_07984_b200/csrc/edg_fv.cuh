@@ -60,10 +60,19 @@ struct FvSmem {
   static constexpr int M = Pde<KIND, DIM>::M;
   static constexpr int NPARTS = KIND == EDG_PDE_EULER ? 3 : 0;
   static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + DIM) + sizeof(unsigned long long) * DIM;
+  // persistent grid kernel: + raw staging of the next patch (interior + 2d halo layers)
+  static constexpr int RAW = M * FvCfg<DIM, K>::NC + 2 * DIM * M * FvCfg<DIM, K>::NL;
+  static constexpr size_t PIPE_BYTES = ((BYTES + 15) / 16) * 16 + 16 + sizeof(double) * RAW;
 };
 
-template <int KIND, int DIM, int K, int MINB = FvCfg<DIM, K>::MINB>
-__global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(const FvArgs A) {
+// One patch b.  PIPE = false: states read from global memory (one CTA per
+// patch).  PIPE = true: states read from the raw staging block sRaw, which the
+// persistent kernel below fills with cp.async while the previous patch is
+// being updated; `after_stage` runs right after the staging barrier (the
+// persistent kernel issues the next patch's copies there).
+template <int KIND, int DIM, int K, bool PIPE, typename AfterStage>
+__device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, double* smem, const double* sRaw,
+                                              AfterStage after_stage) {
   using P = Pde<KIND, DIM>;
   using Cf = FvCfg<DIM, K>;
   constexpr int M = P::M;
@@ -73,7 +82,6 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
   // ext strides: last axis 1, then KEZ, then KEZ*KE
   auto estride = [](int ax) { return ax == DIM - 1 ? 1 : (ax == DIM - 2 ? KEZ : KEZ * KE); };
 
-  extern __shared__ __align__(16) double smem[];
   double* sQ = smem;                               // [M][NE]
   double* sInv = sQ + M * NE;                      // [NE] (Euler)
   double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler)
@@ -81,7 +89,6 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
   unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sC + (EULER ? NE : 0));
   double* sCoef = reinterpret_cast<double*>(sLam + DIM);   // [DIM] dt / (edge / K)
 
-  const int b = blockIdx.x;
   const int tid = threadIdx.x;
   if (tid < DIM) sLam[tid] = 0ull;
   const double* src = A.patch + (size_t)b * M * NC;
@@ -147,7 +154,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
   for (int u = 0; u < NIT; ++u) {
     const int c = tid + u * THREADS;
 #pragma unroll
-    for (int k = 0; k < M; ++k) qi_[u][k] = c < NC ? __ldg(src + k * NC + c) : 0.0;
+    for (int k = 0; k < M; ++k) qi_[u][k] = c < NC ? (PIPE ? sRaw[k * NC + c] : __ldg(src + k * NC + c)) : 0.0;
   }
 #pragma unroll
   for (int u = 0; u < NHT; ++u) {
@@ -167,7 +174,10 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
 #pragma unroll
       for (int ax = 0; ax < DIM; ++ax) x += (ax == a ? (s ? K + 1 : 0) : e[ax] + 1) * estride(ax);
       xh_[u] = x;
-      if (A.halos) {
+      if (PIPE) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) qh_[u][k] = sRaw[M * NC + (fs * M + k) * NL + f];
+      } else if (A.halos) {
 #pragma unroll
         for (int k = 0; k < M; ++k) qh_[u][k] = __ldg(A.halos + (((size_t)b * 2 * DIM + fs) * M + k) * NL + f);
       } else {
@@ -205,6 +215,7 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
   // dt / dx_a, once per CTA (kernels.py:241: dt / (h / k) with exact divisions)
   if (tid < DIM) sCoef[tid] = __ddiv_rn(*A.dt, __ddiv_rn(A.edges[tid], (double)K));
   __syncthreads();
+  after_stage();
 
   // ---- own volumes (CPT consecutive along the last axis) ----
   const int c0 = tid * CPT;
@@ -268,9 +279,11 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
       if (A.status && !finite) atomicAdd(A.status + 1, 1u);
       if (A.dt_slots) {
         const auto pr = P::parts(o[j], A.pp);
+        double l[DIM];
+        P::lam_all(o[j], pr, A.pp, l);
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-          const unsigned long long key = maxkey(P::lam(o[j], pr, a, A.pp));
+          const unsigned long long key = maxkey(l[a]);
           lk[a] = key > lk[a] ? key : lk[a];
         }
       }
@@ -298,6 +311,72 @@ __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(
         atomicMin(A.dt_slots + (b % EDG_DT_SLOTS),
                   (unsigned long long)__double_as_longlong(dt_candidate(A.h_cell, 0, lam)));
     }
+  }
+}
+
+template <int KIND, int DIM, int K, int MINB = FvCfg<DIM, K>::MINB>
+__global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(const FvArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  fv_patch_body<KIND, DIM, K, false>(A, blockIdx.x, smem, nullptr, [] {});
+}
+
+// Persistent patch-grid kernel (edg_fv_grid_step): CTAs walk patches
+// blockIdx.x, blockIdx.x + gridDim.x, ...; the next patch's interior (one
+// contiguous block, 16-byte cp.async) and its 2d halo layers (the neighbour
+// patches' boundary layers, or the own layer at an outflow side) are copied
+// into the raw staging block while the current patch is updated, so the
+// global-load latency is off the critical path.  Same arithmetic and bits as
+// fv_patch_kernel.
+template <int KIND, int DIM, int K>
+__global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_grid_pipe_kernel(const FvArgs A) {
+  using Cf = FvCfg<DIM, K>;
+  using Sm = FvSmem<KIND, DIM, K>;
+  constexpr int M = Pde<KIND, DIM>::M;
+  constexpr int NC = Cf::NC, NL = Cf::NL, THREADS = Cf::THREADS;
+  extern __shared__ __align__(16) double smem[];
+  double* const sRaw = smem + (Sm::BYTES + 7) / 8;   // after the patch block (16-byte aligned below)
+  double* const raw = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sRaw) + 15) & ~uintptr_t(15));
+  const int tid = threadIdx.x;
+  const int n = A.pgrid_n;
+  auto issue = [&](int b) {
+    // interior: contiguous [M][NC] block
+    cp_block<THREADS>(raw, A.patch + (size_t)b * M * NC, M * NC, tid);
+    // halos [2d][M][NL]
+    for (int e = tid; e < 2 * DIM * M * NL; e += THREADS) {
+      const int fs = e / (M * NL), r = e - fs * (M * NL);
+      const int k = r / NL, f = r - k * NL;
+      const int a = fs >> 1, s = fs & 1;
+      int ee[DIM], t = f;
+#pragma unroll
+      for (int ax = DIM - 1; ax >= 0; --ax) {
+        if (ax == a) continue;
+        ee[ax] = t % K;
+        t /= K;
+      }
+      int stride = 1;
+#pragma unroll
+      for (int ax = DIM - 1; ax > a; --ax) stride *= n;
+      const int ia = (b / stride) % n;
+      int j = ia + (s ? 1 : -1);
+      if (j < 0 || j >= n) j = A.periodic ? (j < 0 ? n - 1 : 0) : -1;
+      const int nb = j < 0 ? -1 : b + (j - ia) * stride;
+      ee[a] = nb >= 0 ? (s == 0 ? K - 1 : 0) : (s == 0 ? 0 : K - 1);
+      int c = 0;
+#pragma unroll
+      for (int ax = 0; ax < DIM; ++ax) c = c * K + ee[ax];
+      cp_async8(raw + M * NC + e, A.patch + (size_t)(nb >= 0 ? nb : b) * M * NC + (size_t)k * NC + c);
+    }
+    cp_async_commit();
+  };
+  int b = blockIdx.x;
+  if (b < A.npatches) issue(b);
+  for (; b < A.npatches; b += gridDim.x) {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();   // this patch's raw block has landed; the previous patch is done with smem
+    const int nxt = b + gridDim.x;
+    fv_patch_body<KIND, DIM, K, true>(A, b, smem, raw, [&] {
+      if (nxt < A.npatches) issue(nxt);   // raw block consumed by the staging pass
+    });
   }
 }
 

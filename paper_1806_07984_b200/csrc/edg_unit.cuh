@@ -249,6 +249,22 @@ static int launch_fv_k(const FvArgs& a, cudaStream_t st) {
     const char* v = getenv("EDG_FV_MINB");
     return v ? atoi(v) : 0;
   }();
+  // patch grids (edg_fv_grid_step): persistent kernel with cp.async prefetch
+  // of the next patch (EDG_FV_PIPE=0 selects the one-CTA-per-patch kernel)
+  static const bool pipe = [] {
+    const char* v = getenv("EDG_FV_PIPE");
+    return !(v && v[0] == '0');
+  }();
+  if (pipe && a.pgrid_n > 0 && !a.halos && !a.nbr) {
+    using Sm = FvSmem<KIND, DIM, K>;
+    auto pk = fv_grid_pipe_kernel<KIND, DIM, K>;
+    if (set_smem(pk, Sm::PIPE_BYTES)) return EDG_ERR_CUDA;
+    const int cap = persistent_grid(pk, FvCfg<DIM, K>::THREADS, Sm::PIPE_BYTES);
+    if (cap < 0) return EDG_ERR_CUDA;
+    const int grid = a.npatches < cap ? a.npatches : cap;
+    if (grid > 0) pk<<<grid, FvCfg<DIM, K>::THREADS, Sm::PIPE_BYTES, st>>>(a);
+    return check_launch();
+  }
   auto kern = (minb == 2) ? fv_patch_kernel<KIND, DIM, K, 2> : fv_patch_kernel<KIND, DIM, K>;
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
   if (a.npatches > 0) kern<<<a.npatches, FvCfg<DIM, K>::THREADS, smem, st>>>(a);
