@@ -27,7 +27,7 @@ struct CorrPipe {
   static constexpr int TB = (CPB * TRC + 1) & ~1;
   static constexpr int STAGE = QE + 3 * TB;               // q_end, trace_q, trace_f, neighbour trace_q
   static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TB + 2 * DIM * N) +
-                                  sizeof(unsigned long long) * (DIM * CPB + CPB);
+                                  sizeof(unsigned long long) * (1 + CPB) + sizeof(unsigned) * 2 * DIM * CPB;
 };
 
 template <int KIND, int DIM, int N>
@@ -42,8 +42,9 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
   double* const sStage = smem;                          // [2][STAGE]
   double* const sJump = smem + 2 * C::STAGE;            // [CPB][2d][M][NF]
   double* const sV = sJump + C::TB;                     // [2d][N] lift vectors (uniform cells)
-  unsigned long long* const sLam = reinterpret_cast<unsigned long long*>(sV + 2 * DIM * N);   // [DIM][CPB]
-  unsigned long long* const sFlag = sLam + DIM * CPB;   // [CPB] non-finite flags
+  unsigned long long* const sLam = reinterpret_cast<unsigned long long*>(sV + 2 * DIM * N);   // [1] CTA lambda max
+  unsigned long long* const sFlag = sLam + 1;           // [CPB] non-finite flags
+  unsigned* const sNan = reinterpret_cast<unsigned*>(sFlag + CPB);   // [2][DIM][CPB] NaN-axis flags
 
   const int tid = threadIdx.x;
   const int slot = tid / NPC;
@@ -58,8 +59,9 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
     const double sg = s ? 1.0 : -1.0;
     sV[i] = __ddiv_rn(__dmul_rn(sg, tr), __dmul_rn(A.basis[EDG_BASIS_W(N) + j], A.edges[a]));
   }
-  for (int i = tid; i < DIM * CPB; i += THREADS) sLam[i] = 0ull;
+  if (tid == 0) *sLam = 0ull;
   for (int i = tid; i < CPB; i += THREADS) sFlag[i] = 0ull;
+  for (int i = tid; i < 2 * DIM * CPB; i += THREADS) sNan[i] = 0u;
 
   // per-thread constants: node coordinates, face point of the node on each
   // axis, and the lane mask of this thread's cell segment
@@ -77,8 +79,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
       fpt[a] = (node / (st * N)) * st + (node % st);
     }
   }
-  const unsigned segmask = lane_range_mask(slot * NPC, (slot + 1) * NPC);
-  FastDiv fdn, fdn2;
+    FastDiv fdn, fdn2;
   fdn.init((unsigned)n);
   fdn2.init((unsigned)n * (unsigned)(DIM == 3 ? n : 1));
 
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
     }
   };
 
-  unsigned long long best = DT_EMPTY;   // per-CTA dt candidate (threads < CPB)
+  double lam_run = 0.0;                 // running max of lam_cell over this thread's cells
   unsigned int nonfinite = 0u;
 
   int g = blockIdx.x;
@@ -180,46 +181,59 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
         finite = finite && (fabs(qn[k]) <= 1.7976931348623157e308);
       }
     }
-    if (A.dt_slots) {
-      unsigned long long lk[DIM];
+    // next-step dt: on a uniform grid every cell shares h, so the minimum of
+    // the per-cell candidates h / ((2p+1) lam_cell) is the candidate of the
+    // largest lam_cell (division and the positive scaling are monotone, the
+    // bits are the same).  lam_cell = python max over the axes whose
+    // NaN-propagating node max is not NaN (kernels.py:267-281); an axis is
+    // NaN for the cell iff some node's lambda on it is NaN, which a per-cell,
+    // per-axis shared flag records.  Each node then folds max over its cell's
+    // non-NaN axes into a per-thread running max (no per-group reduction).
+    double lnode[DIM];
+    unsigned* const nanf = sNan + (it & 1) * DIM * CPB;
+    if (A.dt_slots && has_cell) {
       const auto pr = P::parts(qn, A.pp);
+      P::lam_all(qn, pr, A.pp, lnode);
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) lk[a] = 0ull;
-      if (has_cell) {
-        double l[DIM];
-        P::lam_all(qn, pr, A.pp, l);
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) lk[a] = maxkey(l[a]);
-      }
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) seg_max_redux(sLam + a * CPB, has_cell ? slot : -1, segmask, lk[a]);
+      for (int a = 0; a < DIM; ++a)
+        if (lnode[a] != lnode[a]) nanf[a * CPB + slot] = 1u;
     }
     if (has_cell && !finite) sFlag[slot] = 1ull;
     __syncthreads();
+    if (A.dt_slots && has_cell) {
+      double lam = 0.0;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+        if (nanf[a * CPB + slot] == 0u) lam = python_max(lam, lnode[a]);
+      lam_run = lam > lam_run ? lam : lam_run;
+    }
     if (tid < CPB) {
       const int c = g * CPB + tid;
-      if (c < A.ncells) {
-        if (sFlag[tid]) ++nonfinite;
-        if (A.dt_slots) {
-          double lam = 0.0;
-#pragma unroll
-          for (int a = 0; a < DIM; ++a) lam = python_max(lam, from_maxkey(sLam[a * CPB + tid]));
-          if (lam > 0.0) {
-            const unsigned long long cand =
-                (unsigned long long)__double_as_longlong(dt_candidate(A.hmin[0], A.order, lam));
-            best = cand < best ? cand : best;
-          }
-        }
-      }
+      if (c < A.ncells && sFlag[tid]) ++nonfinite;
       sFlag[tid] = 0ull;
+      // the other parity's flags are next written after this group's barriers
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) sLam[a * CPB + tid] = 0ull;
+      for (int a = 0; a < DIM; ++a) sNan[((it + 1) & 1) * DIM * CPB + a * CPB + tid] = 0u;
     }
   }
   cp_async_wait1();   // (only empty groups can be outstanding here)
-  if (tid < CPB) {
-    if (A.status && nonfinite) atomicAdd(A.status + 1, nonfinite);
-    if (A.dt_slots && best != DT_EMPTY) atomicMin(A.dt_slots + (blockIdx.x * CPB + tid) % EDG_DT_SLOTS, best);
+  if (tid < CPB && A.status && nonfinite) atomicAdd(A.status + 1, nonfinite);
+  if (A.dt_slots) {
+    // CTA max of the running maxima (non-negative, NaN-free: bit order = value order)
+    unsigned long long key = (unsigned long long)__double_as_longlong(lam_run);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long v = __shfl_xor_sync(0xffffffffu, key, o);
+      key = v > key ? v : key;
+    }
+    if ((tid & 31) == 0 && key) atomicMax(sLam, key);
+    __syncthreads();
+    if (tid == 0) {
+      const double lam = __longlong_as_double((long long)*sLam);
+      if (lam > 0.0)
+        atomicMin(A.dt_slots + blockIdx.x % EDG_DT_SLOTS,
+                  (unsigned long long)__double_as_longlong(dt_candidate(A.hmin[0], A.order, lam)));
+    }
   }
 }
 

@@ -51,7 +51,7 @@ struct CorrSmem {
   using C = CorrCfg<DIM, N>;
   static constexpr int M = Pde<KIND, DIM>::M;
   static constexpr size_t BYTES = sizeof(double) * (C::CPB * 2 * DIM * M * C::NF + C::CPB * 2 * DIM * N) +
-                                  sizeof(unsigned long long) * (C::CPB * DIM + C::CPB);
+                                  sizeof(unsigned long long) * (C::CPB * DIM + C::CPB) + sizeof(unsigned) * DIM * C::CPB;
 };
 
 template <int KIND, int DIM, int N, bool FUSED>
@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
 
   if (tid < CPB * DIM) sLam[tid] = 0ull;
   if (tid < CPB) sBest[tid] = 0ull;   // doubles as the per-cell non-finite flag until phase 3
+  if (tid < CPB * DIM) reinterpret_cast<unsigned*>(sBest + CPB)[tid] = 0u;   // NaN-axis flags
   // q_end of this node, prefetched so its loads overlap the face gathers
   double qn[M];
   const size_t cb = (size_t)cell * M * NPC;
@@ -195,21 +196,18 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       finite = finite && (fabs(qn[k]) <= 1.7976931348623157e308);
     }
   }
-  if (A.dt_slots) {
-    // per-cell per-axis max wave speed of the new state ([DIM][CPB] keys)
-    unsigned long long lk[DIM];
+  // next-step dt candidate (kernels.py:267-281): lam_cell = python max over
+  // the axes whose NaN-propagating node max is not NaN.  A per-(axis, cell)
+  // shared flag records NaN axes; every node then contributes the max over
+  // its cell's non-NaN axes, and one NaN-free maximum per cell remains.
+  double lnode[DIM];
+  unsigned* const sNan = reinterpret_cast<unsigned*>(sBest + CPB);   // [DIM][CPB]
+  if (A.dt_slots && has_cell) {
     const auto pr = P::parts(qn, A.pp);
+    P::lam_all(qn, pr, A.pp, lnode);
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) lk[a] = 0ull;
-    if (has_cell) {
-      double l[DIM];
-      P::lam_all(qn, pr, A.pp, l);
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) lk[a] = maxkey(l[a]);
-    }
-    const unsigned segmask = lane_range_mask(slot * NPC, (slot + 1) * NPC);
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) seg_max_redux(sLam + a * CPB, has_cell ? slot : -1, segmask, lk[a]);
+    for (int a = 0; a < DIM; ++a)
+      if (lnode[a] != lnode[a]) sNan[a * CPB + slot] = 1u;
   }
   // per-cell non-finite flag (counted once per cell)
   if (has_cell && !finite) atomicOr(reinterpret_cast<unsigned int*>(sBest + slot), 1u);
@@ -219,27 +217,48 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       atomicAdd(A.status + 1, 1u);
   }
   if (A.dt_slots) {
-    __syncthreads();
-    // phase 3: per-cell lambda (python max over axes) -> candidate -> slot min
-    if (tid < CPB) {
-      unsigned long long best = DT_EMPTY;
-      const int c = blockIdx.x * CPB + tid;
-      if (c < A.ncells) {
-        double lam = 0.0;
+    double lam = 0.0;
+    if (has_cell) {
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) lam = python_max(lam, from_maxkey(sLam[a * CPB + tid]));
-        if (lam > 0.0) {
-          const double h = A.hmin[A.edges_per_cell ? c : 0];
-          best = (unsigned long long)__double_as_longlong(dt_candidate(h, A.order, lam));
-        }
-      }
-      sBest[tid] = best;
+      for (int a = 0; a < DIM; ++a)
+        if (sNan[a * CPB + slot] == 0u) lam = python_max(lam, lnode[a]);
     }
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long b = DT_EMPTY;
-      for (int i = 0; i < CPB; ++i) b = sBest[i] < b ? sBest[i] : b;
-      if (b != DT_EMPTY) atomicMin(A.dt_slots + (blockIdx.x % EDG_DT_SLOTS), b);
+    const unsigned long long key = (unsigned long long)__double_as_longlong(lam);   // lam >= 0, no NaN
+    if (A.edges_per_cell == 0) {
+      // uniform h: min over cells of h/((2p+1) lam_cell) = candidate of the CTA max
+      unsigned long long k2 = key;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, k2, o);
+        k2 = v > k2 ? v : k2;
+      }
+      if ((tid & 31) == 0 && k2) atomicMax(sLam, k2);
+      __syncthreads();
+      if (tid == 0) {
+        const double lmax = __longlong_as_double((long long)*sLam);
+        if (lmax > 0.0)
+          atomicMin(A.dt_slots + (blockIdx.x % EDG_DT_SLOTS),
+                    (unsigned long long)__double_as_longlong(dt_candidate(A.hmin[0], A.order, lmax)));
+      }
+    } else {
+      const unsigned segmask = lane_range_mask(slot * NPC, (slot + 1) * NPC);
+      seg_max_redux(sLam, has_cell ? slot : -1, segmask, key);
+      __syncthreads();
+      if (tid < CPB) {
+        unsigned long long best = DT_EMPTY;
+        const int c = blockIdx.x * CPB + tid;
+        if (c < A.ncells) {
+          const double lc = __longlong_as_double((long long)sLam[tid]);
+          if (lc > 0.0) best = (unsigned long long)__double_as_longlong(dt_candidate(A.hmin[c], A.order, lc));
+        }
+        sBest[tid] = best;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long b = DT_EMPTY;
+        for (int i = 0; i < CPB; ++i) b = sBest[i] < b ? sBest[i] : b;
+        if (b != DT_EMPTY) atomicMin(A.dt_slots + (blockIdx.x % EDG_DT_SLOTS), b);
+      }
     }
   }
 }

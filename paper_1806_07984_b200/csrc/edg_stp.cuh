@@ -112,6 +112,11 @@ struct StpSmem {
 #ifndef EDG_STP_SPAD
 #define EDG_STP_SPAD 0
 #endif
+  // EDG_STP_CH2=1: two interleaved FMA chains per derivative dot product
+#ifndef EDG_STP_CH2
+#define EDG_STP_CH2 0
+#endif
+  static constexpr bool CH2 = EDG_STP_CH2;
   static constexpr int SS0 = DIM * M * NPCP;
   static constexpr int SS = (EDG_STP_SPAD && C::CPB > 1) ? SS0 + ((8 - SS0 % 16) + 16) % 16 : SS0;
   static constexpr int FB = C::CPB * SS;                        // one flux buffer
@@ -315,12 +320,34 @@ stp_picard_kernel(const StpArgs A) {
         if ((a == DIM - 1 || (Sm::T0 && a == 0)) && (N % 2 == 0)) {
           // contiguous pencil: 16-byte pair loads (lanes of one pencil broadcast)
 #pragma unroll
-          for (int j = 0; j + 1 < N; j += 2) {
-            const double2 v = *reinterpret_cast<const double2*>(Fa + j);
-            acc_ak = fma(Dr[a][j], v.x, acc_ak);
-            acc_ak = fma(Dr[a][j + 1], v.y, acc_ak);
+          if constexpr (Sm::CH2) {
+            // two interleaved chains (even / odd j): half the dependent-FMA depth
+            double acc_b = 0.0;
+#pragma unroll
+            for (int j = 0; j + 1 < N; j += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(Fa + j);
+              acc_ak = fma(Dr[a][j], v.x, acc_ak);
+              acc_b = fma(Dr[a][j + 1], v.y, acc_b);
+            }
+            if (N & 1) acc_ak = fma(Dr[a][N - 1], Fa[N - 1], acc_ak);
+            acc_ak += acc_b;
+          } else {
+#pragma unroll
+            for (int j = 0; j + 1 < N; j += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(Fa + j);
+              acc_ak = fma(Dr[a][j], v.x, acc_ak);
+              acc_ak = fma(Dr[a][j + 1], v.y, acc_ak);
+            }
+            if (N & 1) acc_ak = fma(Dr[a][N - 1], Fa[N - 1], acc_ak);
           }
-          if (N & 1) acc_ak = fma(Dr[a][N - 1], Fa[N - 1], acc_ak);
+        } else if constexpr (Sm::CH2) {
+          double acc_b = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            if (j & 1) acc_b = fma(Dr[a][j], Fa[j * st], acc_b);
+            else acc_ak = fma(Dr[a][j], Fa[j * st], acc_ak);
+          }
+          acc_ak += acc_b;
         } else {
 #pragma unroll
           for (int j = 0; j < N; ++j) acc_ak = fma(Dr[a][j], Fa[j * st], acc_ak);

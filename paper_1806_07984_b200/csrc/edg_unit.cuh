@@ -249,11 +249,13 @@ static int launch_fv_k(const FvArgs& a, cudaStream_t st) {
     const char* v = getenv("EDG_FV_MINB");
     return v ? atoi(v) : 0;
   }();
-  // patch grids (edg_fv_grid_step): persistent kernel with cp.async prefetch
-  // of the next patch (EDG_FV_PIPE=0 selects the one-CTA-per-patch kernel)
+  // patch grids (edg_fv_grid_step): EDG_FV_PIPE=1 selects the persistent
+  // kernel with cp.async prefetch of the next patch
+  // (measured 9 % slower on cfg4: 2 instead of 3 CTAs per SM and the halo
+  // gather's index arithmetic outweigh the hidden load latency; opt-in)
   static const bool pipe = [] {
     const char* v = getenv("EDG_FV_PIPE");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   if (pipe && a.pgrid_n > 0 && !a.halos && !a.nbr) {
     using Sm = FvSmem<KIND, DIM, K>;
