@@ -27,7 +27,7 @@ struct CorrPipe {
   static constexpr int TB = (CPB * TRC + 1) & ~1;
   static constexpr int STAGE = QE + 3 * TB;               // q_end, trace_q, trace_f, neighbour trace_q
   static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TB + 2 * DIM * N) +
-                                  sizeof(unsigned long long) * (1 + CPB) + sizeof(unsigned) * 2 * DIM * CPB;
+                                  sizeof(unsigned long long) * (1 + CPB + 2) + sizeof(unsigned) * (((2 * DIM * CPB + 1) & ~1));
 };
 
 template <int KIND, int DIM, int N>
@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
   unsigned long long* const sLam = reinterpret_cast<unsigned long long*>(sV + 2 * DIM * N);   // [1] CTA lambda max
   unsigned long long* const sFlag = sLam + 1;           // [CPB] non-finite flags
   unsigned* const sNan = reinterpret_cast<unsigned*>(sFlag + CPB);   // [2][DIM][CPB] NaN-axis flags
+  unsigned long long* const sBar = reinterpret_cast<unsigned long long*>(sNan + ((2 * DIM * CPB + 1) & ~1));   // [2] stage mbarriers
 
   const int tid = threadIdx.x;
   const int slot = tid / NPC;
@@ -85,12 +86,32 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
 
   // issue the copies of group g into stage buffer st; the neighbour face
   // blocks (M * NF contiguous doubles each) go one warp per block
-  auto load_group = [&](int g, double* st) {
+  // The three contiguous blocks go through the bulk-copy (TMA) engine when
+  // 16-byte aligned and sized (one instruction each, completion counted on
+  // the stage's mbarrier); otherwise cooperative cp.async.
+  auto load_group = [&](int g, double* st, unsigned long long* bar) {
     const int c0 = g * CPB;
     const int nc = min(CPB, A.ncells - c0);
-    cp_block<THREADS>(st, A.q_end + (size_t)c0 * M * NPC, nc * M * NPC, tid);
-    cp_block<THREADS>(st + C::QE, A.trace_q + (size_t)c0 * TRC, nc * TRC, tid);
-    cp_block<THREADS>(st + C::QE + C::TB, A.trace_f + (size_t)c0 * TRC, nc * TRC, tid);
+    const double* srcs[3] = {A.q_end + (size_t)c0 * M * NPC, A.trace_q + (size_t)c0 * TRC,
+                             A.trace_f + (size_t)c0 * TRC};
+    double* dsts[3] = {st, st + C::QE, st + C::QE + C::TB};
+    const int cnt[3] = {nc * M * NPC, nc * TRC, nc * TRC};
+    unsigned bulk_bytes = 0;
+    bool bulk[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      bulk[i] = ((reinterpret_cast<uintptr_t>(srcs[i]) & 15) == 0) && ((cnt[i] * 8) % 16 == 0);
+      if (bulk[i]) bulk_bytes += (unsigned)cnt[i] * 8u;
+    }
+    if (tid == 0) {
+      mbar_arrive_expect_tx(bar, bulk_bytes);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        if (bulk[i]) bulk_g2s(dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (!bulk[i]) cp_block<THREADS>(dsts[i], srcs[i], cnt[i], tid);
     double* nq = st + C::QE + 2 * C::TB;
     constexpr int BLK = M * NF;
     constexpr int NW = THREADS / 32;
@@ -120,15 +141,22 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_
   double lam_run = 0.0;                 // running max of lam_cell over this thread's cells
   unsigned int nonfinite = 0u;
 
+  if (tid == 0) {
+    mbar_init(sBar, 1);
+    mbar_init(sBar + 1, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   int g = blockIdx.x;
-  if (g < ngroups) load_group(g, sStage);
+  if (g < ngroups) load_group(g, sStage, sBar);
   cp_async_commit();
   for (int it = 0; g < ngroups; g += gridDim.x, ++it) {
     double* const cur = sStage + (it & 1) * C::STAGE;
     const int gn = g + gridDim.x;
-    if (gn < ngroups) load_group(gn, sStage + ((it + 1) & 1) * C::STAGE);
+    if (gn < ngroups) load_group(gn, sStage + ((it + 1) & 1) * C::STAGE, sBar + ((it + 1) & 1));
     cp_async_commit();
-    cp_async_wait1();
+    cp_async_wait1();                          // own cp.async copies of this group
+    mbar_wait(sBar + (it & 1), (it >> 1) & 1);  // bulk copies of this group
     __syncthreads();
 
     const int cell = g * CPB + slot;

@@ -1,0 +1,84 @@
+"""The kernel variants selected by environment switches (read once per
+process by the library) run the same parity cases as the defaults, each in a
+subprocess:
+
+* EDG_STP_PEN=1   pencil-formulation 2-D STP (edg_stp_pen.cuh): the cfg2 9x9
+                  reference trajectory (CFL 0.2) within 1e-10 and identical
+                  Picard counts;
+* EDG_CORR_PIPE=0 one-CTA-per-group corrector on 2-D grids instead of the
+                  pipelined one: bitwise equal to the default;
+* EDG_CORR_PIPE=1 pipelined corrector on 3-D grids: bitwise equal;
+* EDG_FV_PIPE=1   persistent FV grid kernel: bitwise equal (16^3 volumes, 5 steps).
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_RUN = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r})
+import paper_1806_07984_b200 as edg
+kind = {kind!r}
+g = np.load({golden!r})
+if kind == "dg":
+    tag = {tag!r}
+    N, dim, p, periodic, steps, cells, wlo = (int(v) for v in g[tag + "_meta"])
+    base = {{"cfg2s": "cfg2", "cfg3w": "cfg3"}}[tag]
+    cfg = edg.configs.CONFIGS[base].with_(cfl=float(g[tag + "_cfl"]))
+    pde = edg.pde.make_pde(cfg.pde, dim=cfg.dim)
+    mesh = edg.mesh.CartesianMesh(N, cfg.dim, bool(periodic), extent=N / cells)
+    s = edg.solver.DGSolver(pde, cfg.order, mesh, cfg.cfl)
+    s.set_state(g[tag + "_q0"])
+    s.run(steps, graph=False)
+    s.check_status()
+    np.savez({out!r}, q=s.state().cpu().numpy(), its=s.iterations.cpu().numpy(), dt=s.dt_history())
+else:
+    cfg = edg.configs.CONFIGS["cfg4"]
+    s = edg.solver.FVSolver(edg.pde.euler(3), 16, 8, cfg.cfl)
+    s.set_state(g["cfg4p_q0"])
+    s.run(5, graph=False)
+    s.check_status()
+    np.savez({out!r}, q=s.state().cpu().numpy(), its=np.zeros(1), dt=s.dt_history())
+"""
+
+
+def _run(tmp_path, env_kv, kind, tag=""):
+    out = str(tmp_path / f"{kind}_{tag}_{'_'.join(f'{k}{v}' for k, v in env_kv.items()) or 'default'}.npz")
+    code = _RUN.format(repo=REPO, kind=kind, tag=tag, out=out,
+                       golden=os.path.join(REPO, "tests", "golden", "traj.npz"))
+    env = dict(os.environ)
+    for k in ("EDG_STP_PEN", "EDG_CORR_PIPE", "EDG_FV_PIPE"):
+        env.pop(k, None)
+    env.update(env_kv)
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    return np.load(out)
+
+
+def test_pencil_stp_vs_reference(tmp_path):
+    g = np.load(os.path.join(REPO, "tests", "golden", "traj.npz"))
+    r = _run(tmp_path, {"EDG_STP_PEN": "1"}, "dg", "cfg2s")
+    q = g["cfg2s_q"]
+    assert np.max(np.abs(r["q"] - q)) / np.max(np.abs(q)) <= 1e-10
+    assert np.array_equal(r["its"], g["cfg2s_its"][-1])
+
+
+@pytest.mark.parametrize("tag,env", [("cfg2s", {"EDG_CORR_PIPE": "0"}), ("cfg3w", {"EDG_CORR_PIPE": "1"})])
+def test_corrector_variants_bitwise(tmp_path, tag, env):
+    a = _run(tmp_path, {}, "dg", tag)
+    b = _run(tmp_path, env, "dg", tag)
+    assert np.array_equal(a["q"], b["q"])
+    assert np.array_equal(a["dt"], b["dt"])
+
+
+def test_fv_pipe_bitwise(tmp_path):
+    a = _run(tmp_path, {}, "fv")
+    b = _run(tmp_path, {"EDG_FV_PIPE": "1"}, "fv")
+    assert np.array_equal(a["q"], b["q"])
+    assert np.array_equal(a["dt"], b["dt"])
