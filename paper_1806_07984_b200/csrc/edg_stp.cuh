@@ -123,10 +123,16 @@ struct StpSmem {
   static constexpr int SS = (EDG_STP_SPAD && C::CPB > 1) ? SS0 + ((8 - SS0 % 16) + 16) % 16 : SS0;
   static constexpr int FB = C::CPB * SS;                        // one flux buffer
   // time nodes per pipeline stage (one barrier per stage); EDG_STP_G overrides
-#ifdef EDG_STP_G
+#if defined(EDG_STP_G)
   static constexpr int G = EDG_STP_G;
 #else
-  static constexpr int G = DIM == 2 ? 2 : 1;
+#ifndef EDG_STP_G2D
+#define EDG_STP_G2D 2
+#endif
+#ifndef EDG_STP_G3D
+#define EDG_STP_G3D 1
+#endif
+  static constexpr int G = DIM == 2 ? EDG_STP_G2D : EDG_STP_G3D;
 #endif
   // EDG_STP_QHS: keep the Picard iterate qhat in (thread-private) shared
   // memory instead of registers (fewer registers, more resident CTAs)
@@ -136,7 +142,10 @@ struct StpSmem {
   static constexpr bool QHS = false;
 #endif
   static constexpr int QH = QHS ? C::CPB * N * M * C::NPC : 0;
-  static constexpr size_t BYTES = sizeof(double) * (OPS + 2 * G * FB + 2 * C::CPB * M * C::NPC + QH) + sizeof(int) * 2 * C::CPB;
+  // flux stages: double-buffered groups of G time nodes, or one stage holding
+  // all time nodes when G >= N
+  static constexpr int STAGES = G >= N ? 1 : 2;
+  static constexpr size_t BYTES = sizeof(double) * (OPS + STAGES * G * FB + 2 * C::CPB * M * C::NPC + QH) + sizeof(int) * 2 * C::CPB;
 };
 
 template <int KIND, int DIM, int N, int MINB = StpCfg<DIM, N>::MINB>
@@ -163,7 +172,7 @@ stp_picard_kernel(const StpArgs A) {
   double* sBs = sC + N;              // sum_s B[r][s]
   double* sF = smem + Sm::OPS;       // flux buffers [2][CPB][DIM][M][NPCP], 16-byte aligned (OPS even)
   static_assert(Sm::OPS % 2 == 0 && Sm::OPS >= 2 * N * N + 5 * N, "operator block must keep sF 16-byte aligned");
-  double* sQ0 = sF + 2 * Sm::G * Sm::FB;                       // initial state [2][CPB][M][NPC] (thread-private)
+  double* sQ0 = sF + Sm::STAGES * Sm::G * Sm::FB;                       // initial state [2][CPB][M][NPC] (thread-private)
   double* sQH = sQ0 + 2 * CPB * M * NPC;                      // qhat [CPB][N][M][NPC] when Sm::QHS
   int* sFlag = reinterpret_cast<int*>(sQH + Sm::QH);          // [2][CPB] "not converged" flags
 
@@ -457,7 +466,9 @@ stp_picard_kernel(const StpArgs A) {
         }
       if (!below) flag[slot] = 1;
     }
-    __syncthreads();
+    // one barrier: the flags become visible, and the CTA goes on iff some
+    // active cell has a lane not below tol (that cell stays active)
+    const bool any = __syncthreads_or(active && !below);
     if (active) {
       its = it;
       if (flag[slot] == 0) {
@@ -465,8 +476,10 @@ stp_picard_kernel(const StpArgs A) {
         conv = true;
       }
     }
+    // the other parity was last read before this barrier and is next written
+    // after the next iteration's first barrier
     if (tid < CPB) sFlag[((it + 1) & 1) * CPB + tid] = 0;
-    if (!__syncthreads_or(active)) break;
+    if (!any) break;
   }
 
   // ---------------------------------------------------------- epilogue --

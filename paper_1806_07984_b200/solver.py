@@ -279,7 +279,16 @@ class DGSolver(_Base):
             def enclave_phase():
                 _lib.check(self._stp(self.encl, int(self.encl.numel())), "stp_picard(enclave)")
 
-            if self.two_streams:
+            if tm is not None:
+                # timed (benchmark) order on one stream -- all predictors, then
+                # the faces: same results bitwise, the events bracket the kernels
+                tm.begin("stp")
+                _lib.check(self._stp(self.skel, int(self.skel.numel())), "stp_picard(skeleton)")
+                _lib.check(self._stp(self.encl, int(self.encl.numel())), "stp_picard(enclave)")
+                tm.end("stp")
+                self._faces(0, nsk)
+                self._restrict()
+            elif self.two_streams:
                 main = torch.cuda.current_stream()
                 self.s_hi.wait_stream(main)
                 self.s_lo.wait_stream(main)
@@ -293,12 +302,16 @@ class DGSolver(_Base):
                 skeleton_phase()
                 enclave_phase()
             self._faces(nsk, F - nsk)
+            if tm:
+                tm.begin("corrector")
             _lib.check(lib.edg_corrector(C.byref(self.native), self.order, _lib.ptr(self.table), self.ncells,
                                          _lib.ptr(self.q_end), _lib.ptr(self.trace_q), _lib.ptr(self.trace_f),
                                          None, _lib.ptr(self.side_face), _lib.ptr(self.outcomes),
                                          _lib.ptr(self.edges), self.edges_per_cell, _lib.ptr(self.Qn),
                                          _lib.ptr(self.slots), _lib.ptr(self.hmin), _lib.ptr(self.status),
                                          _stream()), "corrector")
+            if tm:
+                tm.end("corrector")
         self.Q, self.Qn = self.Qn, self.Q
 
 
