@@ -21,7 +21,15 @@ template <int KIND, int DIM, int N>
 struct CorrPipe {
   using Cf = CorrCfg<DIM, N>;
   static constexpr int M = Pde<KIND, DIM>::M;
-  static constexpr int NPC = Cf::NPC, NF = Cf::NF, CPB = Cf::CPB, THREADS = Cf::THREADS;
+  static constexpr int NPC = Cf::NPC, NF = Cf::NF;
+  // cells per group: the classic kernel's count, except one cell per group
+  // when a cell already fills most of a 128-thread CTA (3-D p=4: 125 nodes),
+  // so that two stages of the larger 3-D blocks still leave 4 CTAs per SM
+#ifndef EDG_CORR_PIPE_TARGET
+#define EDG_CORR_PIPE_TARGET 256
+#endif
+  static constexpr int CPB = NPC >= 96 ? 1 : (EDG_CORR_PIPE_TARGET / NPC > 0 ? EDG_CORR_PIPE_TARGET / NPC : 1);
+  static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32 < 64 ? 64 : ((CPB * NPC + 31) / 32) * 32;
   static constexpr int TRC = 2 * DIM * M * NF;            // trace doubles per cell (one family)
   static constexpr int QE = (CPB * M * NPC + 1) & ~1;     // stage sub-blocks, even -> 16-byte aligned
   static constexpr int TB = (CPB * TRC + 1) & ~1;
@@ -31,7 +39,7 @@ struct CorrPipe {
 };
 
 template <int KIND, int DIM, int N>
-__global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_grid_pipe_kernel(const CorrArgs A) {
+__global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_grid_pipe_kernel(const CorrArgs A) {
   using P = Pde<KIND, DIM>;
   using C = CorrPipe<KIND, DIM, N>;
   constexpr int M = C::M, NPC = C::NPC, NF = C::NF, CPB = C::CPB, THREADS = C::THREADS, TRC = C::TRC;

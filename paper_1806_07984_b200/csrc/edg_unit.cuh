@@ -173,11 +173,11 @@ static int launch_corr_grid_n(const CorrArgs& a, cudaStream_t st) {
 template <int N>
 static int launch_corr_n(bool fused, const CorrArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
-  // default: pipelined on 2-D (measured +8% on cfg2), classic on 3-D (the
-  // pipelined 3-D p=4 kernel fits fewer CTAs per SM: measured 7% slower)
+  // default: the pipelined kernel (measured +17 % on cfg2, +24 % on cfg3 with
+  // one cell per group); EDG_CORR_PIPE=0 selects the one-CTA-per-group kernel
   static const bool pipe = [] {
     const char* v = getenv("EDG_CORR_PIPE");
-    return v ? v[0] != '0' : DIM == 2;
+    return v ? v[0] != '0' : true;
   }();
   if (fused && a.grid_n > 0 && a.edges_per_cell == 0 && pipe) return launch_corr_grid_n<N>(a, st);
   using Cf = CorrCfg<DIM, N>;

@@ -5,9 +5,8 @@ subprocess:
 * EDG_STP_PEN=1   pencil-formulation 2-D STP (edg_stp_pen.cuh): the cfg2 9x9
                   reference trajectory (CFL 0.2) within 1e-10 and identical
                   Picard counts;
-* EDG_CORR_PIPE=0 one-CTA-per-group corrector on 2-D grids instead of the
-                  pipelined one: bitwise equal to the default;
-* EDG_CORR_PIPE=1 pipelined corrector on 3-D grids: bitwise equal;
+* EDG_CORR_PIPE=0 one-CTA-per-group corrector instead of the pipelined one
+                  (2-D and 3-D grids): bitwise equal to the default;
 * EDG_FV_PIPE=1   persistent FV grid kernel: bitwise equal (16^3 volumes, 5 steps).
 """
 import os
@@ -69,7 +68,7 @@ def test_pencil_stp_vs_reference(tmp_path):
     assert np.array_equal(r["its"], g["cfg2s_its"][-1])
 
 
-@pytest.mark.parametrize("tag,env", [("cfg2s", {"EDG_CORR_PIPE": "0"}), ("cfg3w", {"EDG_CORR_PIPE": "1"})])
+@pytest.mark.parametrize("tag,env", [("cfg2s", {"EDG_CORR_PIPE": "0"}), ("cfg3w", {"EDG_CORR_PIPE": "0"})])
 def test_corrector_variants_bitwise(tmp_path, tag, env):
     a = _run(tmp_path, {}, "dg", tag)
     b = _run(tmp_path, env, "dg", tag)
