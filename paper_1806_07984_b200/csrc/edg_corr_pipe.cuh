@@ -17,7 +17,7 @@
 
 namespace edg {
 
-template <int KIND, int DIM, int N>
+template <int KIND, int DIM, int N, bool GRID = true>
 struct CorrPipe {
   using Cf = CorrCfg<DIM, N>;
   static constexpr int M = Pde<KIND, DIM>::M;
@@ -33,15 +33,20 @@ struct CorrPipe {
   static constexpr int TRC = 2 * DIM * M * NF;            // trace doubles per cell (one family)
   static constexpr int QE = (CPB * M * NPC + 1) & ~1;     // stage sub-blocks, even -> 16-byte aligned
   static constexpr int TB = (CPB * TRC + 1) & ~1;
-  static constexpr int STAGE = QE + 3 * TB;               // q_end, trace_q, trace_f, neighbour trace_q
-  static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TB + 2 * DIM * N) +
-                                  sizeof(unsigned long long) * (1 + CPB + 2) + sizeof(unsigned) * (((2 * DIM * CPB + 1) & ~1));
+  // grid: q_end, trace_q, trace_f, neighbour trace_q;  adaptive: q_end,
+  // trace_f, face outcomes (gathered through side_face)
+  static constexpr int NB = GRID ? 3 : 2;
+  static constexpr int STAGE = QE + NB * TB;
+  static constexpr int NV = GRID ? 2 * DIM * N : CPB * 2 * DIM * N;    // lift vectors (per cell when adaptive)
+  static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TB + NV) +
+                                  sizeof(unsigned long long) * (1 + CPB + CPB + 2) +
+                                  sizeof(unsigned) * (((2 * DIM * CPB + 1) & ~1));
 };
 
-template <int KIND, int DIM, int N>
-__global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_grid_pipe_kernel(const CorrArgs A) {
+template <int KIND, int DIM, int N, bool GRID = true>
+__global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) corrector_grid_pipe_kernel(const CorrArgs A) {
   using P = Pde<KIND, DIM>;
-  using C = CorrPipe<KIND, DIM, N>;
+  using C = CorrPipe<KIND, DIM, N, GRID>;
   constexpr int M = C::M, NPC = C::NPC, NF = C::NF, CPB = C::CPB, THREADS = C::THREADS, TRC = C::TRC;
   constexpr int FPC = 2 * DIM * M * NF;     // neighbour doubles per cell (= TRC)
   constexpr int TOT = 2 * DIM * NF;         // face points per cell
@@ -49,9 +54,10 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
   extern __shared__ __align__(16) double smem[];
   double* const sStage = smem;                          // [2][STAGE]
   double* const sJump = smem + 2 * C::STAGE;            // [CPB][2d][M][NF]
-  double* const sV = sJump + C::TB;                     // [2d][N] lift vectors (uniform cells)
-  unsigned long long* const sLam = reinterpret_cast<unsigned long long*>(sV + 2 * DIM * N);   // [1] CTA lambda max
-  unsigned long long* const sFlag = sLam + 1;           // [CPB] non-finite flags
+  double* const sV = sJump + C::TB;                     // [2d][N] lift vectors (grid) / [CPB][2d][N] (adaptive)
+  unsigned long long* const sLam = reinterpret_cast<unsigned long long*>(sV + C::NV);   // [1] CTA lambda max
+  unsigned long long* const sLamC = sLam + 1;           // [CPB] per-cell lambda (adaptive)
+  unsigned long long* const sFlag = sLamC + CPB;        // [CPB] non-finite flags
   unsigned* const sNan = reinterpret_cast<unsigned*>(sFlag + CPB);   // [2][DIM][CPB] NaN-axis flags
   unsigned long long* const sBar = reinterpret_cast<unsigned long long*>(sNan + ((2 * DIM * CPB + 1) & ~1));   // [2] stage mbarriers
 
@@ -61,14 +67,18 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
   const int n = A.grid_n;
   const int ngroups = (A.ncells + CPB - 1) / CPB;
 
-  for (int i = tid; i < 2 * DIM * N; i += THREADS) {
+  // lift vectors v[a][s][i] = (sign * l_i(s)) / (w_i * h_a)   (kernels.py:190-191)
+  auto lift = [&](int i, const double* e) {
     const int fs = i / N, j = i % N;
     const int a = fs >> 1, s = fs & 1;
     const double tr = A.basis[(s ? EDG_BASIS_TR(N) : EDG_BASIS_TL(N)) + j];
     const double sg = s ? 1.0 : -1.0;
-    sV[i] = __ddiv_rn(__dmul_rn(sg, tr), __dmul_rn(A.basis[EDG_BASIS_W(N) + j], A.edges[a]));
-  }
+    return __ddiv_rn(__dmul_rn(sg, tr), __dmul_rn(A.basis[EDG_BASIS_W(N) + j], e[a]));
+  };
+  if constexpr (GRID)
+    for (int i = tid; i < 2 * DIM * N; i += THREADS) sV[i] = lift(i, A.edges);
   if (tid == 0) *sLam = 0ull;
+  for (int i = tid; i < CPB; i += THREADS) sLamC[i] = 0ull;
   for (int i = tid; i < CPB; i += THREADS) sFlag[i] = 0ull;
   for (int i = tid; i < 2 * DIM * CPB; i += THREADS) sNan[i] = 0u;
 
@@ -100,32 +110,48 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
   auto load_group = [&](int g, double* st, unsigned long long* bar) {
     const int c0 = g * CPB;
     const int nc = min(CPB, A.ncells - c0);
-    const double* srcs[3] = {A.q_end + (size_t)c0 * M * NPC, A.trace_q + (size_t)c0 * TRC,
+    constexpr int NBK = C::NB;   // contiguous blocks: q_end, (trace_q,) trace_f
+    const double* srcs[3] = {A.q_end + (size_t)c0 * M * NPC, GRID ? A.trace_q + (size_t)c0 * TRC : A.trace_f + (size_t)c0 * TRC,
                              A.trace_f + (size_t)c0 * TRC};
     double* dsts[3] = {st, st + C::QE, st + C::QE + C::TB};
     const int cnt[3] = {nc * M * NPC, nc * TRC, nc * TRC};
     unsigned bulk_bytes = 0;
-    bool bulk[3];
+    bool bulk[3] = {false, false, false};
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < NBK; ++i) {
       bulk[i] = ((reinterpret_cast<uintptr_t>(srcs[i]) & 15) == 0) && ((cnt[i] * 8) % 16 == 0);
       if (bulk[i]) bulk_bytes += (unsigned)cnt[i] * 8u;
     }
     if (tid == 0) {
       mbar_arrive_expect_tx(bar, bulk_bytes);
 #pragma unroll
-      for (int i = 0; i < 3; ++i)
+      for (int i = 0; i < NBK; ++i)
         if (bulk[i]) bulk_g2s(dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
     }
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < NBK; ++i)
       if (!bulk[i]) cp_block<THREADS>(dsts[i], srcs[i], cnt[i], tid);
-    double* nq = st + C::QE + 2 * C::TB;
+    double* nq = st + C::QE + (C::NB - 1) * C::TB;
     constexpr int BLK = M * NF;
     constexpr int NW = THREADS / 32;
     const int warp = tid >> 5, lane = tid & 31;
     for (int bi = warp; bi < nc * 2 * DIM; bi += NW) {
       const int sl = bi / (2 * DIM), fs = bi - sl * (2 * DIM);
+      double* dst = nq + (sl * 2 * DIM + fs) * BLK;
+      if constexpr (!GRID) {
+        // adaptive: the face outcome owning this side (missing: NaN in phase 1)
+        const int fidx = __ldg(A.side_face + (size_t)(c0 + sl) * 2 * DIM + fs);
+        if (fidx >= 0) {
+          const double* src = A.outcomes + (size_t)fidx * BLK;
+          if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+            for (int i = lane; i < BLK / 2; i += 32) cp_async16(dst + 2 * i, src + 2 * i);
+            if ((BLK & 1) && lane == 0) cp_async8(dst + BLK - 1, src + BLK - 1);
+          } else {
+            for (int i = lane; i < BLK; i += 32) cp_async8(dst + i, src + i);
+          }
+        }
+        continue;
+      }
       const int a = fs >> 1, s = fs & 1;
       const unsigned cell = (unsigned)(c0 + sl);
       const unsigned q = a == DIM - 1 ? cell : (a == DIM - 2 ? fdn.div(cell) : fdn2.div(cell));
@@ -136,7 +162,6 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
       // neighbour's opposite face, or (outflow) the cell's own trace
       const double* src = j >= 0 ? A.trace_q + (size_t)((int)cell + (j - ia) * stride) * TRC + (size_t)(2 * a + (1 - s)) * BLK
                                  : A.trace_q + (size_t)cell * TRC + (size_t)fs * BLK;
-      double* dst = nq + (sl * 2 * DIM + fs) * BLK;
       if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
         for (int i = lane; i < BLK / 2; i += 32) cp_async16(dst + 2 * i, src + 2 * i);
         if ((BLK & 1) && lane == 0) cp_async8(dst + BLK - 1, src + BLK - 1);
@@ -146,7 +171,9 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
     }
   };
 
-  double lam_run = 0.0;                 // running max of lam_cell over this thread's cells
+  double lam_run = 0.0;                 // running max of lam_cell over this thread's cells (grid)
+  unsigned long long best = DT_EMPTY;   // running minimum candidate (adaptive, threads < CPB)
+  const unsigned segmask = lane_range_mask(slot * NPC, (slot + 1) * NPC);
   unsigned int nonfinite = 0u;
 
   if (tid == 0) {
@@ -171,10 +198,31 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
     const bool has_cell = slot < CPB && cell < A.ncells;
     const double* qe = cur;
     const double* tq = cur + C::QE;
-    const double* tf = cur + C::QE + C::TB;
-    const double* nq = cur + C::QE + 2 * C::TB;
+    const double* tf = cur + C::QE + (GRID ? C::TB : 0);
+    const double* nq = cur + C::QE + (C::NB - 1) * C::TB;
+    if constexpr (!GRID) {
+      // per-cell lift vectors of this group (cell edges may differ)
+      for (int i = tid; i < CPB * 2 * DIM * N; i += THREADS) {
+        const int sl = i / (2 * DIM * N);
+        const int c = g * CPB + sl;
+        if (c < A.ncells) sV[i] = lift(i - sl * 2 * DIM * N, A.edges + (A.edges_per_cell ? (size_t)c * DIM : 0));
+      }
+    }
+    if (!GRID && has_cell) {
+      // phase 1 (adaptive): outcome - trace_f, outcome gathered by side_face
+      for (int f2 = node; f2 < TOT; f2 += NPC) {
+        const int fs = f2 / NF, f = f2 - fs * NF;
+        const int b = slot * TRC + fs * M * NF + f;
+        const bool have = __ldg(A.side_face + (size_t)cell * 2 * DIM + fs) >= 0;
+        if (!have) atomicOr(A.status, 2u);
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          sJump[b + k * NF] =
+              __dsub_rn(have ? nq[b + k * NF] : __longlong_as_double(0x7FF8000000000000ll), tf[b + k * NF]);
+      }
+    }
     // phase 1: Rusanov outcome - trace_f on the 2d faces (corrector_kernel order)
-    if (has_cell) {
+    if (GRID && has_cell) {
       for (int f2 = node; f2 < TOT; f2 += NPC) {
         const int fs = f2 / NF, f = f2 - fs * NF;
         const int a = fs >> 1, s = fs & 1;
@@ -204,7 +252,7 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
       for (int a = 0; a < DIM; ++a) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-          const double v = sV[(2 * a + s) * N + ix[a]];
+          const double v = sV[(GRID ? 0 : slot * 2 * DIM * N) + (2 * a + s) * N + ix[a]];
 #pragma unroll
           for (int k = 0; k < M; ++k)
             qn[k] = __dsub_rn(qn[k], __dmul_rn(v, sJump[slot * TRC + ((2 * a + s) * M + k) * NF + fpt[a]]));
@@ -236,12 +284,27 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
     }
     if (has_cell && !finite) sFlag[slot] = 1ull;
     __syncthreads();
+    double lam = 0.0;
     if (A.dt_slots && has_cell) {
-      double lam = 0.0;
 #pragma unroll
       for (int a = 0; a < DIM; ++a)
         if (nanf[a * CPB + slot] == 0u) lam = python_max(lam, lnode[a]);
       lam_run = lam > lam_run ? lam : lam_run;
+    }
+    if (!GRID && A.dt_slots) {
+      // per-cell h: per-cell candidates (one NaN-free segmented max per cell)
+      seg_max_redux(sLamC, has_cell ? slot : -1, segmask, (unsigned long long)__double_as_longlong(lam));
+      __syncthreads();
+      if (tid < CPB) {
+        const int c = g * CPB + tid;
+        const double lc = __longlong_as_double((long long)sLamC[tid]);
+        if (c < A.ncells && lc > 0.0) {
+          const unsigned long long cand = (unsigned long long)__double_as_longlong(
+              dt_candidate(A.hmin[A.edges_per_cell ? c : 0], A.order, lc));
+          best = cand < best ? cand : best;
+        }
+        sLamC[tid] = 0ull;
+      }
     }
     if (tid < CPB) {
       const int c = g * CPB + tid;
@@ -254,7 +317,9 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N>::THREADS) corrector_gri
   }
   cp_async_wait1();   // (only empty groups can be outstanding here)
   if (tid < CPB && A.status && nonfinite) atomicAdd(A.status + 1, nonfinite);
-  if (A.dt_slots) {
+  if (!GRID) {
+    if (tid < CPB && A.dt_slots && best != DT_EMPTY) atomicMin(A.dt_slots + (blockIdx.x * CPB + tid) % EDG_DT_SLOTS, best);
+  } else if (A.dt_slots) {
     // CTA max of the running maxima (non-negative, NaN-free: bit order = value order)
     unsigned long long key = (unsigned long long)__double_as_longlong(lam_run);
 #pragma unroll

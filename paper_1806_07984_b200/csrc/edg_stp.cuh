@@ -78,7 +78,10 @@ struct StpCfg {
   static constexpr int NF = ipow(N, DIM - 1);
   // 2-D: ~192 threads (cfg2: 5 cells = 180 nodes, two CTAs = 12 warps fill the
   // 168-register budget of an SM); 3-D: one 125-node cell per 128 threads
-  static constexpr int TARGET = 128;
+#ifndef EDG_STP_TARGET
+#define EDG_STP_TARGET 160
+#endif
+  static constexpr int TARGET = EDG_STP_TARGET;
   static constexpr int CPB = stp_best_cpb(NPC, TARGET);
   static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32;
   // resident CTAs per SM requested from ptxas (caps registers per thread)

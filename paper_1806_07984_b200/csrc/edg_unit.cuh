@@ -156,11 +156,11 @@ int EDG_FN(_stp)(int n, const StpArgs& a, cudaStream_t st) {
 
 // uniform-grid corrector: persistent, cp.async double-buffered kernel
 // (edg_corr_pipe.cuh); EDG_CORR_PIPE=0 selects the one-CTA-per-group kernel
-template <int N>
+template <int N, bool GRID>
 static int launch_corr_grid_n(const CorrArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
-  using C = CorrPipe<KIND, DIM, N>;
-  auto kern = corrector_grid_pipe_kernel<KIND, DIM, N>;
+  using C = CorrPipe<KIND, DIM, N, GRID>;
+  auto kern = corrector_grid_pipe_kernel<KIND, DIM, N, GRID>;
   if (set_smem(kern, C::BYTES)) return EDG_ERR_CUDA;
   const int grid_cap = persistent_grid(kern, C::THREADS, C::BYTES);
   if (grid_cap < 0) return EDG_ERR_CUDA;
@@ -179,7 +179,8 @@ static int launch_corr_n(bool fused, const CorrArgs& a, cudaStream_t st) {
     const char* v = getenv("EDG_CORR_PIPE");
     return v ? v[0] != '0' : true;
   }();
-  if (fused && a.grid_n > 0 && a.edges_per_cell == 0 && pipe) return launch_corr_grid_n<N>(a, st);
+  if (pipe && fused && a.grid_n > 0 && a.edges_per_cell == 0) return launch_corr_grid_n<N, true>(a, st);
+  if (pipe && !fused) return launch_corr_grid_n<N, false>(a, st);
   using Cf = CorrCfg<DIM, N>;
   const size_t smem = CorrSmem<KIND, DIM, N>::BYTES;
   const int blocks = (a.ncells + Cf::CPB - 1) / Cf::CPB;

@@ -6,7 +6,8 @@ subprocess:
                   reference trajectory (CFL 0.2) within 1e-10 and identical
                   Picard counts;
 * EDG_CORR_PIPE=0 one-CTA-per-group corrector instead of the pipelined one
-                  (2-D and 3-D grids): bitwise equal to the default;
+                  (2-D and 3-D grids, and the adaptive cfg5 mesh): bitwise
+                  equal to the default;
 * EDG_FV_PIPE=1   persistent FV grid kernel: bitwise equal (16^3 volumes, 5 steps).
 """
 import os
@@ -35,6 +36,14 @@ if kind == "dg":
     s = edg.solver.DGSolver(pde, cfg.order, mesh, cfg.cfl)
     s.set_state(g[tag + "_q0"])
     s.run(steps, graph=False)
+    s.check_status()
+    np.savez({out!r}, q=s.state().cpu().numpy(), its=s.iterations.cpu().numpy(), dt=s.dt_history())
+elif kind == "amr":
+    cfg = edg.configs.CONFIGS["cfg5"].with_(cells=27)
+    mesh = edg.mesh.AdaptiveMesh(edg.configs.amr_cells(cfg), 2, True)
+    s = edg.solver.DGSolver(edg.pde.euler(2), cfg.order, mesh, cfg.cfl)
+    s.set_state(edg.configs.initial_dg_amr(cfg, mesh.cells))
+    s.run(4, graph=False)
     s.check_status()
     np.savez({out!r}, q=s.state().cpu().numpy(), its=s.iterations.cpu().numpy(), dt=s.dt_history())
 else:
@@ -72,6 +81,13 @@ def test_pencil_stp_vs_reference(tmp_path):
 def test_corrector_variants_bitwise(tmp_path, tag, env):
     a = _run(tmp_path, {}, "dg", tag)
     b = _run(tmp_path, env, "dg", tag)
+    assert np.array_equal(a["q"], b["q"])
+    assert np.array_equal(a["dt"], b["dt"])
+
+
+def test_adaptive_corrector_variant_bitwise(tmp_path):
+    a = _run(tmp_path, {}, "amr")
+    b = _run(tmp_path, {"EDG_CORR_PIPE": "0"}, "amr")
     assert np.array_equal(a["q"], b["q"])
     assert np.array_equal(a["dt"], b["dt"])
 
