@@ -173,14 +173,17 @@ static int launch_corr_grid_n(const CorrArgs& a, cudaStream_t st) {
 template <int N>
 static int launch_corr_n(bool fused, const CorrArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
-  // default: the pipelined kernel (measured +17 % on cfg2, +24 % on cfg3 with
-  // one cell per group); EDG_CORR_PIPE=0 selects the one-CTA-per-group kernel
-  static const bool pipe = [] {
+  // uniform grids: the pipelined kernel by default (measured +17 % on cfg2,
+  // +24 % on cfg3 with one cell per group); adaptive meshes: the one-CTA-per-
+  // group kernel by default (cfg5's 13k cells give each persistent CTA about
+  // one group: nothing to overlap, measured 25 % slower pipelined).
+  // EDG_CORR_PIPE=0 / 1 forces the choice for both.
+  static const int pipe = [] {
     const char* v = getenv("EDG_CORR_PIPE");
-    return v ? v[0] != '0' : true;
+    return v ? (v[0] != '0' ? 1 : 0) : -1;
   }();
-  if (pipe && fused && a.grid_n > 0 && a.edges_per_cell == 0) return launch_corr_grid_n<N, true>(a, st);
-  if (pipe && !fused) return launch_corr_grid_n<N, false>(a, st);
+  if (pipe != 0 && fused && a.grid_n > 0 && a.edges_per_cell == 0) return launch_corr_grid_n<N, true>(a, st);
+  if (pipe == 1 && !fused) return launch_corr_grid_n<N, false>(a, st);
   using Cf = CorrCfg<DIM, N>;
   const size_t smem = CorrSmem<KIND, DIM, N>::BYTES;
   const int blocks = (a.ncells + Cf::CPB - 1) / Cf::CPB;
