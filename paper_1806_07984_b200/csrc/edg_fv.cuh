@@ -263,9 +263,13 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   }
 
   // ---- write back, non-finite count, next-step dt candidate ----
-  unsigned long long lk[DIM];
-#pragma unroll
-  for (int a = 0; a < DIM; ++a) lk[a] = 0ull;
+  // The patch is the dt unit (admissible_dt with order 0 over its volumes):
+  // per axis a NaN-propagating max over the volumes, then the python max over
+  // the axes (NaN axes dropped, kernels.py:267-281).  NaN axes are flagged in
+  // shared memory first; then one NaN-free maximum over volumes and the
+  // remaining axes is reduced (one warp butterfly, one shared atomic per warp).
+  unsigned* const nanbits = reinterpret_cast<unsigned*>(sLam + 1);
+  double lv[CPT][DIM];
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
     const int c = c0 + j;
@@ -279,34 +283,34 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
       if (A.status && !finite) atomicAdd(A.status + 1, 1u);
       if (A.dt_slots) {
         const auto pr = P::parts(o[j], A.pp);
-        double l[DIM];
-        P::lam_all(o[j], pr, A.pp, l);
+        P::lam_all(o[j], pr, A.pp, lv[j]);
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-          const unsigned long long key = maxkey(l[a]);
-          lk[a] = key > lk[a] ? key : lk[a];
-        }
+        for (int a = 0; a < DIM; ++a)
+          if (lv[j][a] != lv[j][a]) atomicOr(nanbits, 1u << a);
       }
-    }
-  }
-  if (A.dt_slots) {
-    // whole CTA is one patch: butterfly max over the warp, one atomic per warp and axis
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const unsigned long long v = __shfl_xor_sync(0xffffffffu, lk[a], off);
-        lk[a] = v > lk[a] ? v : lk[a];
-      }
-      if ((tid & 31) == 0 && lk[a]) atomicMax(sLam + a, lk[a]);
     }
   }
   if (A.dt_slots) {
     __syncthreads();
-    if (tid == 0) {
-      double lam = 0.0;
+    const unsigned nb = *nanbits;
+    double lmax = 0.0;
+    if (ok) {
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) lam = python_max(lam, from_maxkey(sLam[a]));
+      for (int j = 0; j < CPT; ++j)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+          if (!((nb >> a) & 1u)) lmax = lv[j][a] > lmax ? lv[j][a] : lmax;
+    }
+    unsigned long long key = (unsigned long long)__double_as_longlong(lmax);   // >= 0, NaN-free
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long v = __shfl_xor_sync(0xffffffffu, key, off);
+      key = v > key ? v : key;
+    }
+    if ((tid & 31) == 0 && key) atomicMax(sLam, key);
+    __syncthreads();
+    if (tid == 0) {
+      const double lam = __longlong_as_double((long long)*sLam);
       if (lam > 0.0)
         atomicMin(A.dt_slots + (b % EDG_DT_SLOTS),
                   (unsigned long long)__double_as_longlong(dt_candidate(A.h_cell, 0, lam)));
