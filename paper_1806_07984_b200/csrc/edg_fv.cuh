@@ -44,7 +44,16 @@ template <int DIM, int K>
 struct FvCfg {
   static constexpr int NC = ipow(K, DIM);
   static constexpr int KE = K + 2;                      // extended extent (face halos)
-  static constexpr int KEZ = (KE % 2) ? KE : KE + 1;    // last axis padded to an odd length
+  // EDG_FV_Z4=1 (3-D, k = 8): a thread owns volumes z and z+4 of a row and the
+  // last axis is padded to 12, which makes every warp-wide state access
+  // bank-conflict-free (4 lanes per row cover 4 consecutive z, rows land in
+  // disjoint 4-bank-pair blocks); the pressure is then recomputed from the
+  // staged state instead of staged (same operations) to stay at 3 CTAs/SM
+#ifndef EDG_FV_Z4
+#define EDG_FV_Z4 1
+#endif
+  static constexpr bool Z4 = EDG_FV_Z4 && DIM == 3 && K == 8;
+  static constexpr int KEZ = Z4 ? 12 : ((KE % 2) ? KE : KE + 1);    // else: last axis padded to an odd length
   static constexpr int NE = ipow(KE, DIM - 1) * KEZ;    // (bank-conflict-free strided access)
   static constexpr int NL = ipow(K, DIM - 1);           // cells per face layer
 #ifndef EDG_FV_CPT
@@ -58,7 +67,7 @@ struct FvCfg {
 template <int KIND, int DIM, int K>
 struct FvSmem {
   static constexpr int M = Pde<KIND, DIM>::M;
-  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? 3 : 0;
+  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? (FvCfg<DIM, K>::Z4 ? 2 : 3) : 0;
   static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + DIM) + sizeof(unsigned long long) * DIM;
   // persistent grid kernel: + raw staging of the next patch (interior + 2d halo layers)
   static constexpr int RAW = M * FvCfg<DIM, K>::NC + 2 * DIM * M * FvCfg<DIM, K>::NL;
@@ -84,8 +93,9 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
 
   double* sQ = smem;                               // [M][NE]
   double* sInv = sQ + M * NE;                      // [NE] (Euler)
-  double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler)
-  double* sC = sP + (EULER ? NE : 0);              // [NE] (Euler) sound speed
+  constexpr bool Z4 = Cf::Z4 && CPT == 2;
+  double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler; not staged when Z4)
+  double* sC = sP + ((EULER && !Cf::Z4) ? NE : 0); // [NE] (Euler) sound speed
   unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sC + (EULER ? NE : 0));
   double* sCoef = reinterpret_cast<double*>(sLam + DIM);   // [DIM] dt / (edge / K)
 
@@ -115,7 +125,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
     if constexpr (EULER) {
       const auto pr = P::parts(q, A.pp);
       sInv[x] = pr.inv;
-      sP[x] = pr.p;
+      if constexpr (!Cf::Z4) sP[x] = pr.p;
       sC[x] = __dsqrt_rn(__dmul_rn(__dmul_rn(A.pp.gamma, pr.p), pr.inv));
     }
   };
@@ -123,7 +133,19 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
 #pragma unroll
     for (int k = 0; k < M; ++k) s.q[k] = sQ[k * NE + x];
     if constexpr (EULER) {
-      s.pr = {sInv[x], sP[x]};
+      const double inv = sInv[x];
+      double p;
+      if constexpr (Cf::Z4) {
+        // parts() pressure from the staged state and 1/rho (same operations)
+        double ke = __dmul_rn(s.q[1], s.q[1]);
+#pragma unroll
+        for (int i = 1; i < DIM; ++i) ke = __dadd_rn(ke, __dmul_rn(s.q[1 + i], s.q[1 + i]));
+        ke = __dmul_rn(__dmul_rn(0.5, ke), inv);
+        p = __dmul_rn(A.pp.gm1, __dsub_rn(s.q[1 + DIM], ke));
+      } else {
+        p = sP[x];
+      }
+      s.pr = {inv, p};
       s.c = sC[x];
     }
   };
@@ -218,14 +240,16 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   after_stage();
 
   // ---- own volumes (CPT consecutive along the last axis) ----
-  const int c0 = tid * CPT;
+  // volumes c0 + j * DZ: consecutive pairs, or (Z4) z and z + k/2
+  constexpr int DZ = Z4 ? K / 2 : 1;
+  const int c0 = Z4 ? (tid / (K / 2)) * K + tid % (K / 2) : tid * CPT;
   const bool ok = c0 < NC;
   const int x0 = ok ? ext_of_cell(c0) : ext_of_cell(0);
   State me[CPT];
   double o[CPT][M];
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
-    load(x0 + j, me[j]);
+    load(x0 + j * DZ, me[j]);
 #pragma unroll
     for (int k = 0; k < M; ++k) o[j][k] = me[j].q[k];
   }
@@ -233,7 +257,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   for (int a = 0; a < DIM; ++a) {
     const double coef = sCoef[a];
     const int st = estride(a);
-    if (a == DIM - 1 && CPT == 2) {
+    if (a == DIM - 1 && CPT == 2 && !Z4) {
       // interfaces (x0-1 | x0), (x0 | x0+1) shared, (x0+1 | x0+2)
       State nb;
       double fL[M], fM[M], fU[M];
@@ -252,9 +276,9 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
       for (int j = 0; j < CPT; ++j) {
         State nb;
         double fl[M], fh[M];
-        load(x0 + j - st, nb);
+        load(x0 + j * DZ - st, nb);
         iface(nb, me[j], a, fl);
-        load(x0 + j + st, nb);
+        load(x0 + j * DZ + st, nb);
         iface(me[j], nb, a, fh);
 #pragma unroll
         for (int k = 0; k < M; ++k) o[j][k] = __dsub_rn(o[j][k], __dmul_rn(coef, __dsub_rn(fh[k], fl[k])));
@@ -272,7 +296,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   double lv[CPT][DIM];
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
-    const int c = c0 + j;
+    const int c = c0 + j * DZ;
     if (ok) {
       bool finite = true;
 #pragma unroll

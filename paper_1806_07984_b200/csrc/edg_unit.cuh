@@ -3,6 +3,7 @@
 // launchers edg::unit_<name>_*.  Included by edg_k_*.cu with EDG_UNIT_KIND,
 // EDG_UNIT_DIM and EDG_UNIT_NAME defined (split for parallel nvcc builds).
 #include <cstdlib>
+#include <mutex>
 
 #include "edg_stp.cuh"
 #include "edg_stp_th.cuh"
@@ -28,9 +29,11 @@ namespace edg {
 // grid of a persistent kernel: SMs x resident CTAs (cached per kernel)
 template <typename K>
 static int persistent_grid(K kernel, int threads, size_t smem) {
+  static std::mutex mu;
   static const void* keys[64];
   static int vals[64];
   static int used = 0;
+  std::lock_guard<std::mutex> lock(mu);
   for (int i = 0; i < used; ++i)
     if (keys[i] == (const void*)kernel) return vals[i];
   int dev = 0, sms = 0, occ = 0;
