@@ -115,6 +115,11 @@ struct StpSmem {
 #ifndef EDG_STP_SPAD
 #define EDG_STP_SPAD 0
 #endif
+  // with lane quads a warp's 16 distinct words of one axis-0 load fill all
+  // 32 banks only if the two cells of a warp are 16 banks apart
+#ifndef EDG_STP_SPAD_QUAD
+#define EDG_STP_SPAD_QUAD 1
+#endif
   // two interleaved FMA chains per derivative dot product: measured +2 % on
   // 3-D p=4 and -5 % on 2-D p=5, so on by default in 3-D only
   // (EDG_STP_CH2=0/1 forces it)
@@ -122,8 +127,21 @@ struct StpSmem {
 #define EDG_STP_CH2 (-1)
 #endif
   static constexpr bool CH2 = EDG_STP_CH2 < 0 ? DIM == 3 : EDG_STP_CH2 != 0;
+  // EDG_STP_QUAD (default 1): 2x2-node lane quads on 2-D even-N cells
+#ifndef EDG_STP_QUAD
+#define EDG_STP_QUAD 1
+#endif
+  static constexpr bool QUAD = EDG_STP_QUAD && DIM == 2 && N % 2 == 0 && !T0;
+  // EDG_STP_BM (default 1, with QUAD): flux buffers in 2x2-block-major node
+  // order (the lane order), so a warp's flux stores are 32 consecutive words
+  // (bank-conflict-free) and a quad's two words of a load are adjacent
+#ifndef EDG_STP_BM
+#define EDG_STP_BM 1
+#endif
+  static constexpr bool BM = QUAD && EDG_STP_BM;
   static constexpr int SS0 = DIM * M * NPCP;
-  static constexpr int SS = (EDG_STP_SPAD && C::CPB > 1) ? SS0 + ((8 - SS0 % 16) + 16) % 16 : SS0;
+  static constexpr bool SPADX = (EDG_STP_SPAD || (QUAD && EDG_STP_SPAD_QUAD)) && C::CPB > 1;
+  static constexpr int SS = SPADX ? SS0 + ((8 - SS0 % 16) + 16) % 16 : SS0;
   static constexpr int FB = C::CPB * SS;                        // one flux buffer
   // time nodes per pipeline stage (one barrier per stage); EDG_STP_G overrides
 #if defined(EDG_STP_G)
@@ -191,6 +209,18 @@ stp_picard_kernel(const StpArgs A) {
     slot = 0;
     node = v < 0 ? 0 : v;
     lane_ok = v >= 0;
+  } else if constexpr (Sm::QUAD) {
+    // 2-D, even N: lane quad (4 consecutive lanes) = one 2x2 block of nodes,
+    // so every derivative load of a quad touches 2 distinct words (2 rows on
+    // axis 1, 2 columns on axis 0) -- one wavefront per warp-wide LDS.64
+    // instead of two (measured: a quad is served <= 2 distinct addresses per
+    // wavefront)
+    constexpr int HB = N / 2, QPC = HB * HB;
+    const int qd = tid >> 2, u = tid & 3;
+    slot = qd / QPC;
+    const int b = qd - slot * QPC;
+    node = (2 * (b / HB) + (u >> 1)) * N + 2 * (b % HB) + (u & 1);
+    lane_ok = slot < CPB;
   } else {
     slot = tid / NPC;
     node = tid - slot * NPC;
@@ -252,6 +282,19 @@ stp_picard_kernel(const StpArgs A) {
   // transposed axis-0 layout: node (i, j) stored at j * N + i, pencil base j * N
   const int tnode = DIM == 2 ? ix[DIM - 1] * N + ix[0] : 0;
   if constexpr (Sm::T0) pb[0] = ix[DIM - 1] * N;
+  // block-major flux layout: node (r, c) at ((r/2) HB + c/2) 4 + (r%2) 2 + c%2
+  constexpr int HB2 = N / 2;
+  auto bpos = [&](int r, int c) { return ((r >> 1) * HB2 + (c >> 1)) * 4 + (r & 1) * 2 + (c & 1); };
+  const int fnode = Sm::BM ? bpos(ix[0], ix[DIM - 1]) : bnode;
+  if constexpr (Sm::BM) {
+    pb[0] = bpos(0, ix[DIM - 1]);
+    pb[DIM - 1] = bpos(ix[0], 0);
+  }
+  // offset of the j-th node of a pencil along axis a from its base pb[a]
+  auto fofs = [&](int a, int j, int st) {
+    if constexpr (Sm::BM) return a == 0 ? (j >> 1) * HB2 * 4 + (j & 1) * 2 : (j >> 1) * 4 + (j & 1);
+    else return (a == DIM - 1 || (Sm::T0 && a == 0)) ? j : j * st;
+  };
   unsigned its_sum = 0u;
 
   for (int gi = 0; blk < nblocks; blk += gridDim.x, ++gi) {
@@ -316,7 +359,7 @@ stp_picard_kernel(const StpArgs A) {
 #pragma unroll
     for (int a = 0; a < DIM; ++a)
 #pragma unroll
-      for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPCP + ((Sm::T0 && a == 0) ? tnode : bnode)] = F[a][k];
+      for (int k = 0; k < M; ++k) Fb[(a * M + k) * NPCP + ((Sm::T0 && a == 0) ? tnode : fnode)] = F[a][k];
   };
   // dv[k] = sum_a sum_j (D/h_a)[i_a][j] F_a[k][pencil_a(j)]
   auto deriv = [&](const double* Fb, double (&dv)[M]) {
@@ -339,32 +382,32 @@ stp_picard_kernel(const StpArgs A) {
             double acc_b = 0.0;
 #pragma unroll
             for (int j = 0; j + 1 < N; j += 2) {
-              const double2 v = *reinterpret_cast<const double2*>(Fa + j);
+              const double2 v = *reinterpret_cast<const double2*>(Fa + fofs(a, j, st));
               acc_ak = fma(Dr[a][j], v.x, acc_ak);
               acc_b = fma(Dr[a][j + 1], v.y, acc_b);
             }
-            if (N & 1) acc_ak = fma(Dr[a][N - 1], Fa[N - 1], acc_ak);
+            if (N & 1) acc_ak = fma(Dr[a][N - 1], Fa[fofs(a, N - 1, st)], acc_ak);
             acc_ak += acc_b;
           } else {
 #pragma unroll
             for (int j = 0; j + 1 < N; j += 2) {
-              const double2 v = *reinterpret_cast<const double2*>(Fa + j);
+              const double2 v = *reinterpret_cast<const double2*>(Fa + fofs(a, j, st));
               acc_ak = fma(Dr[a][j], v.x, acc_ak);
               acc_ak = fma(Dr[a][j + 1], v.y, acc_ak);
             }
-            if (N & 1) acc_ak = fma(Dr[a][N - 1], Fa[N - 1], acc_ak);
+            if (N & 1) acc_ak = fma(Dr[a][N - 1], Fa[fofs(a, N - 1, st)], acc_ak);
           }
         } else if constexpr (Sm::CH2) {
           double acc_b = 0.0;
 #pragma unroll
           for (int j = 0; j < N; ++j) {
-            if (j & 1) acc_b = fma(Dr[a][j], Fa[j * st], acc_b);
-            else acc_ak = fma(Dr[a][j], Fa[j * st], acc_ak);
+            if (j & 1) acc_b = fma(Dr[a][j], Fa[fofs(a, j, st)], acc_b);
+            else acc_ak = fma(Dr[a][j], Fa[fofs(a, j, st)], acc_ak);
           }
           acc_ak += acc_b;
         } else {
 #pragma unroll
-          for (int j = 0; j < N; ++j) acc_ak = fma(Dr[a][j], Fa[j * st], acc_ak);
+          for (int j = 0; j < N; ++j) acc_ak = fma(Dr[a][j], Fa[fofs(a, j, st)], acc_ak);
         }
         part[a][k] = acc_ak;
       }

@@ -7,6 +7,7 @@
 
 #include "edg_stp.cuh"
 #include "edg_stp_th.cuh"
+#include "edg_stp_pair.cuh"
 #include "edg_stp_pen.cuh"
 #include "edg_stp_ck.cuh"
 #include "edg_faces.cuh"
@@ -75,6 +76,25 @@ static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
       if (set_smem(kern, smem)) return EDG_ERR_CUDA;
       const int blocks = (a.nwork + Ct::CPB - 1) / Ct::CPB;
       if (blocks > 0) kern<<<blocks, Ct::THREADS, smem, st>>>(a);
+      return check_launch();
+    }
+  }
+  if constexpr (DIM == 2 && N % 2 == 0) {
+    // node-pair / time-split kernel (edg_stp_pair.cuh): EDG_STP_PAIR=1 selects it
+    static const int pair = [] {
+      const char* v = getenv("EDG_STP_PAIR");
+      return v ? atoi(v) : 0;
+    }();
+    if (pair) {
+      using Cp = StpPairCfg<N>;
+      const size_t smem = StpPairSmem<KIND, N>::BYTES;
+      auto kern = stp_pair_kernel<KIND, N>;
+      if (set_smem(kern, smem)) return EDG_ERR_CUDA;
+      const int blocks = (a.nwork + Cp::CPB - 1) / Cp::CPB;
+      const int cap = persistent_grid(kern, Cp::THREADS, smem);
+      if (cap < 0) return EDG_ERR_CUDA;
+      const int grid = blocks < cap ? blocks : cap;
+      if (grid > 0) kern<<<grid, Cp::THREADS, smem, st>>>(a);
       return check_launch();
     }
   }
