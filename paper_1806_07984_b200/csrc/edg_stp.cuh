@@ -163,6 +163,12 @@ struct StpSmem {
   static constexpr bool QHS = false;
 #endif
   static constexpr int QH = QHS ? C::CPB * N * M * C::NPC : 0;
+  // EDG_STP_PP (default 1): unroll the Picard loop by two so that qhat and
+  // the next iterate swap register roles instead of being copied
+#ifndef EDG_STP_PP
+#define EDG_STP_PP 1
+#endif
+  static constexpr bool PP = EDG_STP_PP && !QHS;
   // flux stages: double-buffered groups of G time nodes, or one stage holding
   // all time nodes when G >= N
   static constexpr int STAGES = G >= N ? 1 : 2;
@@ -425,107 +431,233 @@ stp_picard_kernel(const StpArgs A) {
     }
   };
 
-  for (int it = 1; it <= max_iter; ++it) {
-    if (it == 1) {
-      // qhat_s = q for every time node (kernels.py:134), so the first
-      // iteration needs one flux and one derivative:
-      //   acc[r] = c_r q + (sum_s B[r][s]) div F(q)
-      if (active) {
-        double q[M];
-        qrow(0, q);
-        put_flux(buf0, q);
-      }
-      __syncthreads();
-      if (active) {
-        double dv[M];
-        deriv(buf0, dv);
+  if constexpr (Sm::PP) {
+    // ping-pong: odd iterations write acc, even ones qhr (no copies); the
+    // latest iterate of this lane's cell is in acc iff inacc
+    bool inacc = false;
+    auto rowof = [&](const double (&qa)[N][M], int r, double (&out)[M]) {
 #pragma unroll
-        for (int k = 0; k < M; ++k) {
-#pragma unroll
-          for (int r = 0; r < N; ++r) acc[r][k] = fma(sBs[r], dv[k], sC[r] * qget(r, k));
+      for (int k = 0; k < M; ++k) out[k] = qa[r][k];
+    };
+    // convergence flags and the CTA-wide continue decision (see below)
+    auto finish = [&](int it, bool below, bool into_acc) -> bool {
+      int* flag = sFlag + (it & 1) * CPB;
+      if (active && !below) flag[slot] = 1;
+      const bool any = __syncthreads_or(active && !below);
+      if (active) {
+        its = it;
+        inacc = into_acc;
+        if (flag[slot] == 0) {
+          active = false;
+          conv = true;
         }
       }
-    } else {
-      // G time nodes per barrier; stage buffers [2][G]
-      constexpr int G = Sm::G;
-      auto slotbuf = [&](int stage, int g) { return buf0 + (stage * G + g) * Sm::FB; };
-      if (active) {
-#pragma unroll
-        for (int k = 0; k < M; ++k) {
-          const double q0 = q0s[k * NPC];
-#pragma unroll
-          for (int r = 0; r < N; ++r) acc[r][k] = sC[r] * q0;
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-          if (g < N) {
-            double q[M];
-            qrow(g, q);
-            put_flux(slotbuf(0, g), q);
-          }
-      }
-      __syncthreads();
-      // software pipeline: the fluxes of the next G time nodes are evaluated
-      // and stored (other stage) while the derivatives of this group are
-      // contracted; one barrier per group
-#pragma unroll
-      for (int s0 = 0; s0 < N; s0 += G) {
-        const int stage = (s0 / G) & 1;
+      if (tid < CPB) sFlag[((it + 1) & 1) * CPB + tid] = 0;
+      return any;
+    };
+    auto body = [&](const double (&qc)[N][M], double (&qn)[N][M], int it, bool into_acc) -> bool {
+        // G time nodes per barrier; stage buffers [2][G]
+        constexpr int G = Sm::G;
+        auto slotbuf = [&](int stage, int g) { return buf0 + (stage * G + g) * Sm::FB; };
         if (active) {
 #pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const double q0 = q0s[k * NPC];
+#pragma unroll
+            for (int r = 0; r < N; ++r) qn[r][k] = sC[r] * q0;
+          }
+#pragma unroll
           for (int g = 0; g < G; ++g)
-            if (s0 + G + g < N) {
+            if (g < N) {
               double q[M];
-              qrow(s0 + G + g, q);
-              put_flux(slotbuf(stage ^ 1, g), q);
+              rowof(qc, g, q);
+              put_flux(slotbuf(0, g), q);
             }
+        }
+        __syncthreads();
+        // software pipeline: the fluxes of the next G time nodes are evaluated
+        // and stored (other stage) while the derivatives of this group are
+        // contracted; one barrier per group
 #pragma unroll
-          for (int g = 0; g < G; ++g) {
-            if (s0 + g < N) {
-              double dv[M];
-              deriv(slotbuf(stage, g), dv);
+        for (int s0 = 0; s0 < N; s0 += G) {
+          const int stage = (s0 / G) & 1;
+          if (active) {
 #pragma unroll
-              for (int r = 0; r < N; ++r) {
-                const double b = sB[r * N + s0 + g];
+            for (int g = 0; g < G; ++g)
+              if (s0 + G + g < N) {
+                double q[M];
+                rowof(qc, s0 + G + g, q);
+                put_flux(slotbuf(stage ^ 1, g), q);
+              }
 #pragma unroll
-                for (int k = 0; k < M; ++k) acc[r][k] = fma(b, dv[k], acc[r][k]);
+            for (int g = 0; g < G; ++g) {
+              if (s0 + g < N) {
+                double dv[M];
+                deriv(slotbuf(stage, g), dv);
+#pragma unroll
+                for (int r = 0; r < N; ++r) {
+                  const double b = sB[r * N + s0 + g];
+#pragma unroll
+                  for (int k = 0; k < M; ++k) qn[r][k] = fma(b, dv[k], qn[r][k]);
+                }
               }
             }
           }
+          __syncthreads();
+        }
+      bool below = true;
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int k = 0; k < M; ++k) below = below & (fabs(qn[r][k] - qc[r][k]) < A.tol);
+      }
+      return finish(it, below, into_acc);
+    };
+    bool any = false;
+    if (max_iter >= 1) {
+        // qhat_s = q for every time node (kernels.py:134), so the first
+        // iteration needs one flux and one derivative:
+        //   acc[r] = c_r q + (sum_s B[r][s]) div F(q)
+        if (active) {
+          double q[M];
+          qrow(0, q);
+          put_flux(buf0, q);
         }
         __syncthreads();
+        if (active) {
+          double dv[M];
+          deriv(buf0, dv);
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+#pragma unroll
+            for (int r = 0; r < N; ++r) acc[r][k] = fma(sBs[r], dv[k], sC[r] * qget(r, k));
+          }
+        }
+      bool below = true;
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int k = 0; k < M; ++k) below = below & (fabs(acc[r][k] - qhr[r][k]) < A.tol);
       }
+      any = finish(1, below, true);
     }
-    // delta = max |acc - qhat| < tol  <=>  every |acc - qhat| < tol (a NaN
-    // fails the comparison exactly as it poisons np.max): a per-thread
-    // predicate (DADD + DSETP.AND per value) and a per-cell "some lane is not
-    // below tol" flag replace the max reduction
-    int* flag = sFlag + (it & 1) * CPB;
-    bool below = true;
-    if (active) {
+    for (int it = 2; any && it <= max_iter;) {
+      any = body(acc, qhr, it, false);
+      if (!any || ++it > max_iter) break;
+      any = body(qhr, acc, it, true);
+      ++it;
+    }
+    if (inacc) {
 #pragma unroll
       for (int r = 0; r < N; ++r)
 #pragma unroll
-        for (int k = 0; k < M; ++k) {
-          below = below & (fabs(acc[r][k] - qget(r, k)) < A.tol);
-          qset(r, k, acc[r][k]);
+        for (int k = 0; k < M; ++k) qhr[r][k] = acc[r][k];
+    }
+  } else {
+    for (int it = 1; it <= max_iter; ++it) {
+      if (it == 1) {
+        // qhat_s = q for every time node (kernels.py:134), so the first
+        // iteration needs one flux and one derivative:
+        //   acc[r] = c_r q + (sum_s B[r][s]) div F(q)
+        if (active) {
+          double q[M];
+          qrow(0, q);
+          put_flux(buf0, q);
         }
-      if (!below) flag[slot] = 1;
-    }
-    // one barrier: the flags become visible, and the CTA goes on iff some
-    // active cell has a lane not below tol (that cell stays active)
-    const bool any = __syncthreads_or(active && !below);
-    if (active) {
-      its = it;
-      if (flag[slot] == 0) {
-        active = false;
-        conv = true;
+        __syncthreads();
+        if (active) {
+          double dv[M];
+          deriv(buf0, dv);
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+#pragma unroll
+            for (int r = 0; r < N; ++r) acc[r][k] = fma(sBs[r], dv[k], sC[r] * qget(r, k));
+          }
+        }
+      } else {
+        // G time nodes per barrier; stage buffers [2][G]
+        constexpr int G = Sm::G;
+        auto slotbuf = [&](int stage, int g) { return buf0 + (stage * G + g) * Sm::FB; };
+        if (active) {
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const double q0 = q0s[k * NPC];
+#pragma unroll
+            for (int r = 0; r < N; ++r) acc[r][k] = sC[r] * q0;
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            if (g < N) {
+              double q[M];
+              qrow(g, q);
+              put_flux(slotbuf(0, g), q);
+            }
+        }
+        __syncthreads();
+        // software pipeline: the fluxes of the next G time nodes are evaluated
+        // and stored (other stage) while the derivatives of this group are
+        // contracted; one barrier per group
+#pragma unroll
+        for (int s0 = 0; s0 < N; s0 += G) {
+          const int stage = (s0 / G) & 1;
+          if (active) {
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+              if (s0 + G + g < N) {
+                double q[M];
+                qrow(s0 + G + g, q);
+                put_flux(slotbuf(stage ^ 1, g), q);
+              }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              if (s0 + g < N) {
+                double dv[M];
+                deriv(slotbuf(stage, g), dv);
+#pragma unroll
+                for (int r = 0; r < N; ++r) {
+                  const double b = sB[r * N + s0 + g];
+#pragma unroll
+                  for (int k = 0; k < M; ++k) acc[r][k] = fma(b, dv[k], acc[r][k]);
+                }
+              }
+            }
+          }
+          __syncthreads();
+        }
       }
+      // delta = max |acc - qhat| < tol  <=>  every |acc - qhat| < tol (a NaN
+      // fails the comparison exactly as it poisons np.max): a per-thread
+      // predicate (DADD + DSETP.AND per value) and a per-cell "some lane is not
+      // below tol" flag replace the max reduction
+      int* flag = sFlag + (it & 1) * CPB;
+      bool below = true;
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            below = below & (fabs(acc[r][k] - qget(r, k)) < A.tol);
+            qset(r, k, acc[r][k]);
+          }
+        if (!below) flag[slot] = 1;
+      }
+      // one barrier: the flags become visible, and the CTA goes on iff some
+      // active cell has a lane not below tol (that cell stays active)
+      const bool any = __syncthreads_or(active && !below);
+      if (active) {
+        its = it;
+        if (flag[slot] == 0) {
+          active = false;
+          conv = true;
+        }
+      }
+      // the other parity was last read before this barrier and is next written
+      // after the next iteration's first barrier
+      if (tid < CPB) sFlag[((it + 1) & 1) * CPB + tid] = 0;
+      if (!any) break;
     }
-    // the other parity was last read before this barrier and is next written
-    // after the next iteration's first barrier
-    if (tid < CPB) sFlag[((it + 1) & 1) * CPB + tid] = 0;
-    if (!any) break;
   }
 
   // ---------------------------------------------------------- epilogue --
