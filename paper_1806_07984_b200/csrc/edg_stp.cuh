@@ -72,6 +72,14 @@ static __constant__ int kStpPerm3d5[128] = {
     113, 14, 39, 64, 89, 114, 120, -1, 18, 43, 68, 93, 118, 19, 44, 69, 94, 119, 23, 48, 73, 98,
     123, 24, 49, 74, 99, 124, 21, 46, 71, 96, 121, 22, 47, 72, 97, 122, -1, -1};
 
+// constant-bank copy of the basis table head (D, w, tl, tr, K^-1, K^-1 lift)
+// for N = 2..8 at offsets pen_off(N); one copy per instantiation unit, filled
+// by the launchers (device-to-device copy in stream order before the kernel)
+constexpr int pen_ops(int n) { return 2 * n * n + 4 * n; }
+constexpr int pen_off(int n) { return n <= 2 ? 0 : pen_off(n - 1) + pen_ops(n - 1); }
+constexpr int kPenTotal = pen_off(9);
+static __constant__ double kPen[kPenTotal];
+
 template <int DIM, int N>
 struct StpCfg {
   static constexpr int NPC = ipow(N, DIM);
@@ -169,6 +177,17 @@ struct StpSmem {
 #define EDG_STP_PP 1
 #endif
   static constexpr bool PP = EDG_STP_PP && !QHS;
+  // EDG_STP_KC (default 1): the time contraction takes K^-1 from the constant
+  // bank (kPen, an FMA operand: no shared load) and scales the derivative by
+  // (-dt) w_s first -- the reference's own order (kernels.py:141-142)
+  // KC = 1 scales the derivative, KC = 2 scales K^-1 per (r, s) (B bit-identical
+  // to the shared-memory table); measured best: 2 on 2-D (+8 % on cfg2 at CFL
+  // 0.9), 1 on 3-D (+2 % on cfg3)
+#ifndef EDG_STP_KC
+#define EDG_STP_KC (-1)
+#endif
+  static constexpr int KCM = EDG_STP_KC < 0 ? (DIM == 2 ? 2 : 1) : EDG_STP_KC;
+  static constexpr bool KC = KCM != 0 && PP;
   // flux stages: double-buffered groups of G time nodes, or one stage holding
   // all time nodes when G >= N
   static constexpr int STAGES = G >= N ? 1 : 2;
@@ -494,11 +513,28 @@ stp_picard_kernel(const StpArgs A) {
               if (s0 + g < N) {
                 double dv[M];
                 deriv(slotbuf(stage, g), dv);
+                if constexpr (Sm::KC) {
+                  constexpr int O = pen_off(N);
+                  const double sc = -(dt * kPen[O + EDG_BASIS_W(N) + s0 + g]);   // = (-dt) w_s exactly
+                  if constexpr (Sm::KCM == 1) {
 #pragma unroll
-                for (int r = 0; r < N; ++r) {
-                  const double b = sB[r * N + s0 + g];
+                    for (int k = 0; k < M; ++k) dv[k] *= sc;
+                  }
 #pragma unroll
-                  for (int k = 0; k < M; ++k) qn[r][k] = fma(b, dv[k], qn[r][k]);
+                  for (int r = 0; r < N; ++r) {
+                    // KC = 2: B[r][s] = K^-1[r][s] * ((-dt) w_s), bit-identical to sB
+                    const double b = Sm::KCM == 1 ? kPen[O + EDG_BASIS_KINV(N) + r * N + s0 + g]
+                                                     : kPen[O + EDG_BASIS_KINV(N) + r * N + s0 + g] * sc;
+#pragma unroll
+                    for (int k = 0; k < M; ++k) qn[r][k] = fma(b, dv[k], qn[r][k]);
+                  }
+                } else {
+#pragma unroll
+                  for (int r = 0; r < N; ++r) {
+                    const double b = sB[r * N + s0 + g];
+#pragma unroll
+                    for (int k = 0; k < M; ++k) qn[r][k] = fma(b, dv[k], qn[r][k]);
+                  }
                 }
               }
             }

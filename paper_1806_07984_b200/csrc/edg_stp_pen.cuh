@@ -25,12 +25,7 @@
 
 namespace edg {
 
-// constant-bank copy of the basis table head (D, w, tl, tr, K^-1, K^-1 lift)
-// for N = 2..6 at offsets kPenOff(N); one copy per instantiation unit
-constexpr int pen_ops(int n) { return 2 * n * n + 4 * n; }
-constexpr int pen_off(int n) { return n <= 2 ? 0 : pen_off(n - 1) + pen_ops(n - 1); }
-constexpr int kPenTotal = pen_off(7);
-static __constant__ double kPen[kPenTotal];
+// constant-bank basis table kPen: edg_stp.cuh
 
 template <int KIND, int N>
 struct PenCfg {

@@ -59,6 +59,32 @@ static int set_smem(K kernel, size_t bytes) {
   return EDG_OK;
 }
 
+// operator table head of order N -> this unit's constant bank (kPen).  The
+// table is a pure function of N (basis.py packed_table), so it is copied once
+// per process: synchronously (device to device) outside stream capture; inside
+// a capture the copy becomes a node of the graph, in stream order before the
+// kernel, and the next uncaptured call still makes the one-time copy.
+template <int N>
+static int upload_ops(const double* basis, cudaStream_t st) {
+  static std::mutex mu;
+  static bool done = false;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done) return EDG_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return EDG_ERR_CUDA;
+  if (cs != cudaStreamCaptureStatusNone)
+    return cudaMemcpyToSymbolAsync(kPen, basis, sizeof(double) * pen_ops(N), sizeof(double) * pen_off(N),
+                                   cudaMemcpyDeviceToDevice, st) == cudaSuccess ? EDG_OK : EDG_ERR_CUDA;
+  // the basis upload may still be in flight on the caller's stream
+  if (cudaStreamSynchronize(st) != cudaSuccess ||
+      cudaMemcpyToSymbol(kPen, basis, sizeof(double) * pen_ops(N), sizeof(double) * pen_off(N),
+                         cudaMemcpyDeviceToDevice) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess)
+    return EDG_ERR_CUDA;
+  done = true;
+  return EDG_OK;
+}
+
 template <int N>
 static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
@@ -130,6 +156,9 @@ static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
   }();
   auto kern = (minb == 2) ? stp_picard_kernel<KIND, DIM, N, 2> : stp_picard_kernel<KIND, DIM, N>;
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
+  if (StpSmem<KIND, DIM, N>::KC) {
+    if (upload_ops<N>(a.basis, st)) return EDG_ERR_CUDA;
+  }
   const int blocks = (a.nwork + Cf::CPB - 1) / Cf::CPB;
   // persistent CTAs (the kernel strides over work blocks)
   const int cap = persistent_grid(kern, Cf::THREADS, smem);
