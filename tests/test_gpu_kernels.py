@@ -213,3 +213,28 @@ def test_stp_linear_vs_reference_ck_vectors(edg, golden_ops):
             assert rel_linf(st.q_int, g("ck_q_int")[c]) < 1e-12
     with pytest.raises(edg.errors.EnclaveDgError):
         edg.kernels.stp_linear(np.ones((4, 4, 4)), edg.pde.euler(2), 1e-3, edg.basis.get_basis(3), (0.1, 0.1))
+
+
+@pytest.mark.parametrize("n", [1, 31, 729, 59049])
+def test_order_by_iterations_is_descending_permutation(edg, n):
+    """edg_order_by_iterations (counting sort of the cells by their last
+    Picard count, heaviest first): a permutation, counts non-increasing,
+    counts >= 63 share the last bucket."""
+    import torch
+    from paper_1806_07984_b200 import _lib
+    rng = np.random.default_rng(n)
+    its = rng.integers(0, 80, size=n).astype(np.int32)
+    its_d = torch.from_numpy(its).cuda()
+    order = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    scratch = torch.zeros(128, dtype=torch.int32, device="cuda")
+    import ctypes
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for _ in range(2):   # the histogram is left zeroed for the next call
+        _lib.check(_lib.load().edg_order_by_iterations(n, _lib.ptr(its_d), _lib.ptr(order), _lib.ptr(scratch), st),
+                   "order")
+        torch.cuda.synchronize()
+        o = order.cpu().numpy()
+        assert np.array_equal(np.sort(o), np.arange(n))
+        key = np.minimum(its[o], 63)
+        assert np.all(np.diff(key) <= 0)
+        assert not scratch[:64].any()
