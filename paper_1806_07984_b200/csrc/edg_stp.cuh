@@ -59,18 +59,19 @@ constexpr int stp_best_cpb(int npc, int target) {
 }
 
 // Lane -> node map of the 3-D p = 4 kernel (one 125-node cell per 128-thread
-// CTA).  Warp w takes a compact block of (i1, i2) pencil pairs with all five
-// i0 values, so that a warp-wide LDS.64 of a derivative step touches <= 16
-// distinct pencils (one wavefront) on all three axes for warps 0-2 (warp 3:
-// two on axis 1) instead of 25 distinct axis-0 pencils in row-major order
-// (generated and checked by tools/perm3d5.py; -1 = idle lane).
+// CTA), opt-in EDG_STP_PERM3: lane quads are 2x2 'plates' of nodes (warps
+// 0-1: (j,k) plates; warps 2-3: (j,k), (i,k), (i,j) plates and the leftover
+// lines), so that two of the three derivative loads of a quad ask for 2 words
+// split 2+2 (tools/perm/plates3d.py generates and models it; -1 = idle lane).
+// Measured 12 % slower on cfg3: with row-major flux storage the plates raise
+// bank conflicts (LDS.64 2.51 wavefronts, STS.64 4.25, vs 2.32 / 2.0).
 static __constant__ int kStpPerm3d5[128] = {
-    0,  25, 50, 75, 100, 1,  26, 51, 76, 101, 2,   27, 52, 77, 102, 5,  30, 55, 80, 105, 6,  31,
-    56, 81, 106, 7,  32, 57, 82, 107, 20, 45, 10,  35, 60, 85, 110, 11, 36, 61, 86, 111, 12, 37,
-    62, 87, 112, 15, 40, 65, 90, 115, 16, 41, 66,  91, 116, 17, 42, 67, 92, 117, 70, 95, 3,  28,
-    53, 78, 103, 4,  29, 54, 79, 104, 8,  33, 58,  83, 108, 9,  34, 59, 84, 109, 13, 38, 63, 88,
-    113, 14, 39, 64, 89, 114, 120, -1, 18, 43, 68, 93, 118, 19, 44, 69, 94, 119, 23, 48, 73, 98,
-    123, 24, 49, 74, 99, 124, 21, 46, 71, 96, 121, 22, 47, 72, 97, 122, -1, -1};
+    0, 1, 5, 6, 2, 3, 7, 8, 10, 11, 15, 16, 12, 13, 17, 18, 25, 26, 30, 31, 27, 28, 32, 33, 35, 36, 40,
+    41, 37, 38, 42, 43, 50, 51, 55, 56, 52, 53, 57, 58, 60, 61, 65, 66, 62, 63, 67, 68, 75, 76, 80, 81,
+    77, 78, 82, 83, 85, 86, 90, 91, 87, 88, 92, 93, 100, 101, 105, 106, 102, 103, 107, 108, 110, 111,
+    115, 116, 112, 113, 117, 118, 20, 21, 45, 46, 22, 23, 47, 48, 70, 71, 95, 96, 72, 73, 97, 98, 4, 9,
+    29, 34, 14, 19, 39, 44, 54, 59, 79, 84, 64, 69, 89, 94, 120, 121, 122, 123, 104, 109, 114, 119, 24,
+    49, 74, 99, 124, -1, -1, -1};
 
 // constant-bank copy of the basis table head (D, w, tl, tr, K^-1, K^-1 lift)
 // for N = 2..8 at offsets pen_off(N); one copy per instantiation unit, filled
@@ -225,9 +226,11 @@ stp_picard_kernel(const StpArgs A) {
   const int tid = threadIdx.x;
   int slot, node;
   bool lane_ok;
-  // disabled: measured 20% slower on cfg3 (bank conflicts of the compact
-  // blocks outweigh the fewer distinct pencils); kept for reference
-  constexpr bool kUsePerm3d5 = false;
+  // EDG_STP_PERM3=1: the 2x2-plate lane map of tools/perm/plates3d.py
+#ifndef EDG_STP_PERM3
+#define EDG_STP_PERM3 0
+#endif
+  constexpr bool kUsePerm3d5 = EDG_STP_PERM3 != 0;
   if constexpr (kUsePerm3d5 && DIM == 3 && N == 5 && CPB == 1) {
     // compact lane->node blocks: <= 16 distinct pencils per warp on most axes
     const int v = kStpPerm3d5[tid];
