@@ -195,6 +195,28 @@ int edg_fv_grid_step(const edg_pde* pde, int32_t k, int32_t patches_per_axis, in
 int edg_patch_boundary_layers(int32_t dim, int32_t m, int32_t k, int32_t npatches,
                               const double* patch_dev, double* out_dev, void* stream);
 
+/* ---- cell-local operators of dynamic AMR -----
+ * edg_gradient_indicator: transfer.py:136-158 on a batch q (C, m, n^d):
+ *   ind[c] = max over axes (a NaN axis dropped) of max |D-contraction|
+ *   (NaN-propagating over nodes and components); with verdict_dev != NULL
+ *   also the refine (+1) / keep (0) / coarsen (-1) verdict against
+ *   refine_tol > coarsen_tol and level_dev[c] (NULL = level 0) in
+ *   [min_level, max_level] (evaluate_refinement_criterion).
+ * edg_interpolate_volume: transfer.py:99-102; item i maps the parent
+ *   q[parent_dev[i]] (NULL: q[i]) onto the child with per-axis digits
+ *   digits_dev[i][0..dim-1] (int8 [nitems][3]) -> out (nitems, m, n^d).
+ * edg_restrict_volume: transfer.py:105-118; children (P, 3^d, m, n^d) in
+ *   row-major digit order -> out (P, m, n^d). */
+int edg_gradient_indicator(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t ncells,
+                           const double* q_dev, const int32_t* level_dev, double refine_tol, double coarsen_tol,
+                           int32_t max_level, int32_t min_level, double* ind_dev, int8_t* verdict_dev,
+                           void* stream);
+int edg_interpolate_volume(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t nitems,
+                           const int32_t* parent_dev, const double* q_dev, const int8_t* digits_dev,
+                           double* out_dev, void* stream);
+int edg_restrict_volume(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t nparents,
+                        const double* children_dev, double* out_dev, void* stream);
+
 /* ---- measurement helper: fp64 FMA throughput probe ----------------------
  * Launches `blocks` x 256 threads, each running 8 independent DFMA chains of
  * `iters` steps (flops = blocks * 256 * 8 * iters * 2).  Time it with events

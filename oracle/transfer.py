@@ -94,3 +94,28 @@ def restrict_volume(ops: Transfer, children: dict):
         part = along_axes([ops.restrict[j] for j in digits], q, range(1, 1 + d))
         out = part if out is None else out + part
     return out
+
+
+def gradient_indicator(q, order: int) -> float:
+    """transfer.py:136-148: the largest |reference-space derivative| over the
+    nodes, components and axes (np.max per axis propagates NaN, the Python
+    max over axes drops a NaN axis)."""
+    D = basis_for(order).diff_matrix
+    worst = 0.0
+    for ax in range(q.ndim - 1):
+        g = np.moveaxis(np.tensordot(D, q, axes=(1, 1 + ax)), 0, 1 + ax)
+        worst = max(worst, float(np.abs(g).max()))
+    return worst
+
+
+REFINE, KEEP, COARSEN = 1, 0, -1
+
+
+def refinement_verdict(q, level, order, refine_tol, coarsen_tol, max_level, min_level) -> int:
+    """transfer.py:151-158 as +1 refine / 0 keep / -1 coarsen."""
+    ind = gradient_indicator(q, order)
+    if ind > refine_tol and level < max_level:
+        return REFINE
+    if ind < coarsen_tol and level > min_level:
+        return COARSEN
+    return KEEP

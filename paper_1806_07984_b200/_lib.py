@@ -56,6 +56,9 @@ SIGNATURES = {
     "edg_fv_grid_step": (C.c_int, [PDEP, I32, I32, I32, P, P, P, P, P, D, P, P]),
     "edg_patch_boundary_layers": (C.c_int, [I32, I32, I32, I32, P, P, P]),
     "edg_stream_priority_range": (C.c_int, [C.POINTER(I32), C.POINTER(I32)]),
+    "edg_gradient_indicator": (C.c_int, [I32, I32, I32, P, I32, P, P, D, D, I32, I32, P, P, P]),
+    "edg_interpolate_volume": (C.c_int, [I32, I32, I32, P, I32, P, P, P, P, P]),
+    "edg_restrict_volume": (C.c_int, [I32, I32, I32, P, I32, P, P, P]),
 }
 
 _LIB = None

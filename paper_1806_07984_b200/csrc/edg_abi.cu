@@ -4,11 +4,13 @@
 // reference's error contract as status codes (errors.py:4-33).
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "edg_stp.cuh"
 #include "edg_faces.cuh"
 #include "edg_fv.cuh"
 #include "edg_dt.cuh"
+#include "edg_amr.cuh"
 
 namespace edg {
 #define EDG_DECL_UNIT(name)                                                                                  \
@@ -510,6 +512,115 @@ int edg_stream_priority_range(int32_t* least, int32_t* greatest) {
   *least = lo;
   *greatest = hi;
   return EDG_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------- dynamic AMR, cell-local ops --
+template <int DIM, typename F>
+static int amr_dispatch(int n, F f) {
+  switch (n) {
+#define EDG_CASE(NN) \
+  case NN:           \
+    return f(std::integral_constant<int, NN>{});
+    EDG_CASE(2) EDG_CASE(3) EDG_CASE(4) EDG_CASE(5) EDG_CASE(6) EDG_CASE(7) EDG_CASE(8)
+#undef EDG_CASE
+  }
+  return EDG_ERR_CONFIG;
+}
+
+template <typename K>
+static int amr_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024 &&
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return EDG_ERR_CUDA;
+  return EDG_OK;
+}
+
+template <int DIM>
+static int indicator_dim(int n, const double* basis, int m, int nc, const double* q, const int32_t* level,
+                         double rt, double ct, int maxl, int minl, double* ind, int8_t* verdict, cudaStream_t st) {
+  return amr_dispatch<DIM>(n, [&](auto NN) {
+    constexpr int N = decltype(NN)::value;
+    const size_t bytes = sizeof(double) * (N * N + (size_t)m * ipow(N, DIM));
+    auto k = gradient_indicator_kernel<DIM, N>;
+    if (amr_smem(k, bytes)) return (int)EDG_ERR_CUDA;
+    k<<<nc, kAmrThreads, bytes, st>>>(basis, m, nc, q, level, rt, ct, maxl, minl, ind, verdict);
+    return check_launch();
+  });
+}
+
+template <int DIM>
+static int interp_vol_dim(int n, const double* basis, int m, int ni, const int32_t* parent, const double* q,
+                          const int8_t* digits, double* out, cudaStream_t st) {
+  return amr_dispatch<DIM>(n, [&](auto NN) {
+    constexpr int N = decltype(NN)::value;
+    const size_t bytes = sizeof(double) * (3 * N * N + 2 * (size_t)m * ipow(N, DIM));
+    auto k = interpolate_volume_kernel<DIM, N>;
+    if (amr_smem(k, bytes)) return (int)EDG_ERR_CUDA;
+    k<<<ni, kAmrThreads, bytes, st>>>(basis, m, ni, parent, q, digits, out);
+    return check_launch();
+  });
+}
+
+template <int DIM>
+static int restrict_vol_dim(int n, const double* basis, int m, int np, const double* children, double* out,
+                            cudaStream_t st) {
+  return amr_dispatch<DIM>(n, [&](auto NN) {
+    constexpr int N = decltype(NN)::value;
+    const size_t bytes = sizeof(double) * (3 * N * N + 3 * (size_t)m * ipow(N, DIM));
+    auto k = restrict_volume_kernel<DIM, N>;
+    if (amr_smem(k, bytes)) return (int)EDG_ERR_CUDA;
+    k<<<np, kAmrThreads, bytes, st>>>(basis, m, np, children, out);
+    return check_launch();
+  });
+}
+
+extern "C" {
+
+int edg_gradient_indicator(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t ncells,
+                           const double* q_dev, const int32_t* level_dev, double refine_tol, double coarsen_tol,
+                           int32_t max_level, int32_t min_level, double* ind_dev, int8_t* verdict_dev,
+                           void* stream) {
+  if (order < 1 || order > 7) return fail(EDG_ERR_CONFIG, "order out of range");
+  if (m < 1) return fail(EDG_ERR_CONFIG, "m must be positive");
+  // RefinementDecision.__post_init__ (transfer.py:131-133)
+  if (verdict_dev && !(refine_tol > coarsen_tol && coarsen_tol >= 0.0))
+    return fail(EDG_ERR_CONFIG, "need refine_tol > coarsen_tol >= 0 (hysteresis band)");
+  if (ncells <= 0) return EDG_OK;
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (dim == 2)
+    return cuda_status(indicator_dim<2>(order + 1, basis_dev, m, ncells, q_dev, level_dev, refine_tol, coarsen_tol,
+                                        max_level, min_level, ind_dev, verdict_dev, st));
+  if (dim == 3)
+    return cuda_status(indicator_dim<3>(order + 1, basis_dev, m, ncells, q_dev, level_dev, refine_tol, coarsen_tol,
+                                        max_level, min_level, ind_dev, verdict_dev, st));
+  return fail(EDG_ERR_CONFIG, "dim must be 2 or 3");
+}
+
+int edg_interpolate_volume(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t nitems,
+                           const int32_t* parent_dev, const double* q_dev, const int8_t* digits_dev,
+                           double* out_dev, void* stream) {
+  if (order < 1 || order > 7) return fail(EDG_ERR_CONFIG, "order out of range");
+  if (m < 1) return fail(EDG_ERR_CONFIG, "m must be positive");
+  if (nitems <= 0) return EDG_OK;
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (dim == 2)
+    return cuda_status(interp_vol_dim<2>(order + 1, basis_dev, m, nitems, parent_dev, q_dev, digits_dev, out_dev, st));
+  if (dim == 3)
+    return cuda_status(interp_vol_dim<3>(order + 1, basis_dev, m, nitems, parent_dev, q_dev, digits_dev, out_dev, st));
+  return fail(EDG_ERR_CONFIG, "dim must be 2 or 3");
+}
+
+int edg_restrict_volume(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t nparents,
+                        const double* children_dev, double* out_dev, void* stream) {
+  if (order < 1 || order > 7) return fail(EDG_ERR_CONFIG, "order out of range");
+  if (m < 1) return fail(EDG_ERR_CONFIG, "m must be positive");
+  if (nparents <= 0) return EDG_OK;
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (dim == 2) return cuda_status(restrict_vol_dim<2>(order + 1, basis_dev, m, nparents, children_dev, out_dev, st));
+  if (dim == 3) return cuda_status(restrict_vol_dim<3>(order + 1, basis_dev, m, nparents, children_dev, out_dev, st));
+  return fail(EDG_ERR_CONFIG, "dim must be 2 or 3");
 }
 
 }  // extern "C"

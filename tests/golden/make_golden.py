@@ -4,9 +4,10 @@ Run in the build container (the only place /root/reference exists):
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
 
-Writes tests/golden/ops.npz (per-kernel known-answer vectors) and
-tests/golden/traj.npz (short Algorithm-1 trajectories of proxy configs) plus
-tests/golden/mesh_cfg5_proxy.json (face forest of a refined mesh).  Every
+Writes tests/golden/ops.npz (per-kernel known-answer vectors),
+tests/golden/traj.npz (short Algorithm-1 trajectories of proxy configs),
+tests/golden/mesh_cfg5_proxy.json (face forest of a refined mesh) and
+tests/golden/amr.npz (volumetric transfer and refinement criterion, f2).  Every
 number in them comes out of /root/reference/pkg/src/enclavedg; the only
 additions are the Euler PdeDescriptor (the reference has none -- it is built
 here in the reference's own plugin format, pde.py:10-24, from the formulas in
@@ -424,9 +425,48 @@ def gen_traj():
     print("traj.npz + mesh json done")
 
 
+def gen_amr():
+    """SURVEY.md section 8(f) f2, the cell-local part of dynamic AMR:
+    transfer.py:99-158 (interpolate_volume, restrict_volume,
+    gradient_indicator, evaluate_refinement_criterion) on seeded cells."""
+    out = {}
+    rng = np.random.default_rng(20261020)
+    cases = [(2, 3, 4), (2, 5, 4), (3, 4, 5), (2, 1, 1), (3, 2, 5), (2, 7, 4), (3, 5, 1)]
+    out["amr_ncases"] = np.array(len(cases))
+    dec = rt.RefinementDecision(refine_tol=0.5, coarsen_tol=0.05, max_level=3)
+    for ci, (dim, p, m) in enumerate(cases):
+        n = p + 1
+        t = rt.get_transfer(p)
+        C = 5
+        Q = rng.standard_normal((C, m) + (n,) * dim)
+        Q[1] *= 1e-3                      # a smooth, low-indicator cell
+        Q[2] = Q[2, :, :1].repeat(n, axis=1) if dim == 2 else Q[2]
+        pre = f"amr{ci}_"
+        out[pre + "meta"] = np.array([dim, p, m, C])
+        out[pre + "q"] = Q
+        out[pre + "ind"] = np.array([rt.gradient_indicator(Q[c], p) for c in range(C)])
+        levels = np.array([0, 1, 2, 3, 1], dtype=np.int32)
+        out[pre + "levels"] = levels
+        code = {rt.RefinementDecision.REFINE: 1, rt.RefinementDecision.KEEP: 0, rt.RefinementDecision.COARSEN: -1}
+        out[pre + "verdict"] = np.array([code[rt.evaluate_refinement_criterion(Q[c], int(levels[c]), p, dec, 1)]
+                                         for c in range(C)], dtype=np.int8)
+        digits = list(np.ndindex(*(3,) * dim))
+        out[pre + "interp"] = np.stack([rt.interpolate_volume(t, Q[0], dg) for dg in digits])
+        children = {dg: rng.standard_normal((m,) + (n,) * dim) for dg in digits}
+        out[pre + "children"] = np.stack([children[dg] for dg in digits])
+        out[pre + "restrict"] = rt.restrict_volume(t, children)
+        # refine -> coarsen round trip of a parent polynomial (reproduced exactly up to rounding)
+        out[pre + "roundtrip"] = rt.restrict_volume(t, {dg: rt.interpolate_volume(t, Q[3], dg) for dg in digits})
+    out["amr_decision"] = np.array([dec.refine_tol, dec.coarsen_tol, dec.max_level, 1.0])
+    np.savez_compressed(os.path.join(HERE, "amr.npz"), **out)
+    print("amr.npz done")
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["ops", "traj"]
+    what = sys.argv[1:] or ["ops", "traj", "amr"]
     if "ops" in what:
         gen_ops()
     if "traj" in what:
         gen_traj()
+    if "amr" in what:
+        gen_amr()
