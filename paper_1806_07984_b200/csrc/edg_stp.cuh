@@ -81,6 +81,10 @@ constexpr int pen_off(int n) { return n <= 2 ? 0 : pen_off(n - 1) + pen_ops(n - 
 constexpr int kPenTotal = pen_off(9);
 static __constant__ double kPen[kPenTotal];
 
+#ifndef EDG_STP_MAP3
+#define EDG_STP_MAP3 0
+#endif
+
 template <int DIM, int N>
 struct StpCfg {
   static constexpr int NPC = ipow(N, DIM);
@@ -248,6 +252,14 @@ stp_picard_kernel(const StpArgs A) {
     slot = qd / QPC;
     const int b = qd - slot * QPC;
     node = (2 * (b / HB) + (u >> 1)) * N + 2 * (b % HB) + (u & 1);
+    lane_ok = slot < CPB;
+  } else if constexpr (DIM == 3 && CPB == 1 && EDG_STP_MAP3 != 0) {
+    // EDG_STP_MAP3 = 1: lanes run fastest along axis 0 (node (i, j, k) at lane
+    // (j n + k) n + i); = 2: fastest along axis 1 (lane (i n + k) n + j)
+    slot = tid / NPC;
+    const int t = tid - slot * NPC;
+    const int f = t % N, p = t / N;
+    node = EDG_STP_MAP3 == 1 ? f * N * N + p : (p / N) * N * N + f * N + p % N;
     lane_ok = slot < CPB;
   } else {
     slot = tid / NPC;

@@ -2,9 +2,10 @@
 process by the library) run the same parity cases as the defaults, each in a
 subprocess:
 
-* EDG_STP_PEN=1   pencil-formulation 2-D STP (edg_stp_pen.cuh): the cfg2 9x9
-                  reference trajectory (CFL 0.2) within 1e-10 and identical
-                  Picard counts;
+* EDG_STP_PEN=1   pencil-formulation 2-D STP (edg_stp_pen.cuh) and
+  EDG_STP_PAIR=1  node-pair / time-split 2-D STP (edg_stp_pair.cuh): the cfg2
+                  9x9 reference trajectory (CFL 0.2) within 1e-10 and
+                  identical Picard counts;
 * EDG_CORR_PIPE=0 one-CTA-per-group corrector instead of the pipelined one
                   on 2-D and 3-D grids, and EDG_CORR_PIPE=1 the pipelined one
                   on the adaptive cfg5 mesh: bitwise equal to the defaults;
@@ -61,12 +62,22 @@ def _run(tmp_path, env_kv, kind, tag=""):
     code = _RUN.format(repo=REPO, kind=kind, tag=tag, out=out,
                        golden=os.path.join(REPO, "tests", "golden", "traj.npz"))
     env = dict(os.environ)
-    for k in ("EDG_STP_PEN", "EDG_CORR_PIPE", "EDG_FV_PIPE"):
+    for k in ("EDG_STP_PEN", "EDG_STP_PAIR", "EDG_CORR_PIPE", "EDG_FV_PIPE"):
         env.pop(k, None)
     env.update(env_kv)
     p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     return np.load(out)
+
+
+@pytest.mark.parametrize("env", [{"EDG_STP_PAIR": "1"}])
+def test_pair_stp_vs_reference(tmp_path, env):
+    """Node-pair / time-split 2-D predictor (edg_stp_pair.cuh)."""
+    g = np.load(os.path.join(REPO, "tests", "golden", "traj.npz"))
+    r = _run(tmp_path, env, "dg", "cfg2s")
+    q = g["cfg2s_q"]
+    assert np.max(np.abs(r["q"] - q)) / np.max(np.abs(q)) <= 1e-10
+    assert np.array_equal(r["its"], g["cfg2s_its"][-1])
 
 
 def test_pencil_stp_vs_reference(tmp_path):
