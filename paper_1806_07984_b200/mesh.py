@@ -23,6 +23,7 @@ its closure meets the synthetic partition cut x = 0.5.
 from __future__ import annotations
 
 import itertools
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -61,11 +62,32 @@ class CartesianMesh:
         return (self.h,) * self.dim
 
 
+@dataclass
+class MeshDelta:
+    """Topology change between two mesh states (the reference's MeshDelta,
+    mesh.py:104-115).  Face keys are this package's (axis, level, position)
+    leaf-face keys."""
+    created_cells: set = field(default_factory=set)
+    removed_cells: set = field(default_factory=set)
+    created_faces: set = field(default_factory=set)
+    removed_faces: set = field(default_factory=set)
+
+    @property
+    def empty(self):
+        return not (self.created_cells or self.removed_cells or self.created_faces or self.removed_faces)
+
+
 class AdaptiveMesh:
-    def __init__(self, cells, dim: int, periodic: bool, extent: float = 1.0, cut_x=0.5):
+    def __init__(self, cells, dim: int, periodic: bool, extent: float = 1.0, cut_x=0.5, max_depth: int = 10):
         if dim not in (2, 3):
             raise ConfigError(f"dim must be 2 or 3, got {dim}")
         self.dim, self.periodic, self.extent = dim, periodic, extent
+        self.max_depth = max_depth
+        self.version = 0
+        self._init_cells(cells, cut_x)
+
+    def _init_cells(self, cells, cut_x):
+        dim, extent = self.dim, self.extent
         cells = [(int(l), tuple(int(i) for i in ix)) for l, ix in cells]
         self.cells = sorted(cells, key=self._sfc_key)
         self.ncells = len(self.cells)
@@ -79,6 +101,53 @@ class AdaptiveMesh:
 
     def cell_edges(self, level):
         return tuple(self.extent / 3 ** level for _ in range(self.dim))
+
+    # ------------------------------------------------- topology updates --
+    def child_keys(self, key):
+        """The 3^d children of a cell key in the reference's child-digit order
+        (mesh.py:170-181, digits row-major)."""
+        level, idx = key
+        return [(level + 1, tuple(3 * idx[t] + dg[t] for t in range(self.dim)))
+                for dg in itertools.product(range(3), repeat=self.dim)]
+
+    def parent_key(self, key):
+        level, idx = key
+        return None if level == 0 else (level - 1, tuple(i // 3 for i in idx))
+
+    def _face_keys(self):
+        return set(k[1:] for k in self._leaf_keys)
+
+    def update_topology(self, refine_cells=(), coarsen_parents=(), cut_x="keep"):
+        """Refine real cells into their 3^d children and merge fully real
+        3^d clusters into their parents, then rebuild the face forest once
+        (mesh.py:309-317).  Raises ConfigError for an invalid target (the
+        reference's InvalidTargetError / NotCoarsenableError / CapacityError)
+        and for results with more than one level between face neighbours,
+        which this solver does not support.  Returns a MeshDelta."""
+        before_cells, before_faces = set(self.cells), self._face_keys()
+        cells = set(self.cells)
+        for key in refine_cells:
+            if key not in cells:
+                raise ConfigError(f"cannot refine {key}: not a real cell")
+            if key[0] + 1 > self.max_depth:
+                raise ConfigError(f"refinement beyond max depth {self.max_depth}")
+            cells.remove(key)
+            cells.update(self.child_keys(key))
+        for parent in coarsen_parents:
+            kids = self.child_keys(parent)
+            if parent in cells or not all(k in cells for k in kids):
+                raise ConfigError(f"cannot coarsen {parent}: children are not all real cells")
+            cells.difference_update(kids)
+            cells.add(parent)
+        # build the new state first: an invalid result leaves the mesh untouched
+        new = AdaptiveMesh(cells, self.dim, self.periodic, self.extent,
+                           self.cut_x if cut_x == "keep" else cut_x, self.max_depth)
+        version = self.version + 1
+        self.__dict__.update(new.__dict__)
+        self.version = version
+        after_faces = self._face_keys()
+        return MeshDelta(set(self.cells) - before_cells, before_cells - set(self.cells),
+                         after_faces - before_faces, before_faces - after_faces)
 
     def _sfc_key(self, cell):
         level, idx = cell
@@ -162,6 +231,7 @@ class AdaptiveMesh:
         self.enclave = np.nonzero(~self.skeleton_mask)[0].astype(np.int32)
         on_skel = {k: bool(self.skeleton_mask[rec["cells"]].all()) for k, rec in leaf.items()}
         leaf_keys = sorted(leaf, key=lambda k: (not on_skel[k], k[1], k[2], k[3]))
+        self._leaf_keys = leaf_keys
         self.nleaf_skeleton = sum(on_skel.values())
         par_keys = sorted(parents, key=lambda k: (k[1], k[2], k[3]))
         index = {k: i for i, k in enumerate(leaf_keys)}

