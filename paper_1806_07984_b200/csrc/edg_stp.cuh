@@ -98,11 +98,16 @@ struct StpCfg {
   static constexpr int CPB = stp_best_cpb(NPC, TARGET);
   static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32;
   // resident CTAs per SM requested from ptxas (caps registers per thread)
-  // (measured: 2 for the 2-D p=5 kernel, 3 for the 3-D p=4 kernel)
+  // (measured: 2 for the 2-D p=5 kernel; 2 for the 3-D p=4 kernel since the
+  // constant-bank K^-1 and the unrolled Picard loop: 255 registers, 8 warps
+  // per SM, 3 % faster than 3 CTAs at 168 registers)
+#ifndef EDG_STP_MINB_3D
+#define EDG_STP_MINB_3D 2
+#endif
 #ifdef EDG_STP_MINB_2D
-  static constexpr int MINB = DIM == 2 ? EDG_STP_MINB_2D : 3;
+  static constexpr int MINB = DIM == 2 ? EDG_STP_MINB_2D : EDG_STP_MINB_3D;
 #else
-  static constexpr int MINB = DIM == 2 ? 2 : 3;
+  static constexpr int MINB = DIM == 2 ? 2 : EDG_STP_MINB_3D;
 #endif
 };
 
@@ -164,7 +169,7 @@ struct StpSmem {
 #define EDG_STP_G2D 2
 #endif
 #ifndef EDG_STP_G3D
-#define EDG_STP_G3D 1
+#define EDG_STP_G3D 2
 #endif
   static constexpr int G = DIM == 2 ? EDG_STP_G2D : EDG_STP_G3D;
 #endif
