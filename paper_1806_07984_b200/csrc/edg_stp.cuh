@@ -89,10 +89,12 @@ template <int DIM, int N>
 struct StpCfg {
   static constexpr int NPC = ipow(N, DIM);
   static constexpr int NF = ipow(N, DIM - 1);
-  // 2-D: ~192 threads (cfg2: 5 cells = 180 nodes, two CTAs = 12 warps fill the
-  // 168-register budget of an SM); 3-D: one 125-node cell per 128 threads
+  // 2-D: ~100-128 threads per CTA (cfg2: 3 cells = 108 nodes in 128 threads,
+  // cfg5: 6 cells = 96 nodes), 3 CTAs per SM at 168 registers -- measured
+  // faster than 5 cells in 192 threads x 2 CTAs (smaller barrier domains);
+  // 3-D: one 125-node cell per 128 threads
 #ifndef EDG_STP_TARGET
-#define EDG_STP_TARGET 160
+#define EDG_STP_TARGET 100
 #endif
   static constexpr int TARGET = EDG_STP_TARGET;
   static constexpr int CPB = stp_best_cpb(NPC, TARGET);
@@ -104,11 +106,10 @@ struct StpCfg {
 #ifndef EDG_STP_MINB_3D
 #define EDG_STP_MINB_3D 2
 #endif
-#ifdef EDG_STP_MINB_2D
-  static constexpr int MINB = DIM == 2 ? EDG_STP_MINB_2D : EDG_STP_MINB_3D;
-#else
-  static constexpr int MINB = DIM == 2 ? 2 : EDG_STP_MINB_3D;
+#ifndef EDG_STP_MINB_2D
+#define EDG_STP_MINB_2D 3
 #endif
+  static constexpr int MINB = DIM == 2 ? EDG_STP_MINB_2D : EDG_STP_MINB_3D;
 };
 
 template <int KIND, int DIM, int N>
