@@ -172,7 +172,12 @@ struct StpSmem {
 #ifndef EDG_STP_G3D
 #define EDG_STP_G3D 2
 #endif
-  static constexpr int G = DIM == 2 ? EDG_STP_G2D : EDG_STP_G3D;
+  // 2-D n >= 6: all time nodes in one stage (one flux barrier per iteration;
+  // +1.5 % on cfg2), smaller n: pipelined pairs (+6 % on cfg5's n = 4)
+#ifndef EDG_STP_G2D_BIG
+#define EDG_STP_G2D_BIG 8
+#endif
+  static constexpr int G = DIM == 2 ? (N >= 6 ? EDG_STP_G2D_BIG : EDG_STP_G2D) : EDG_STP_G3D;
 #endif
   // EDG_STP_QHS: keep the Picard iterate qhat in (thread-private) shared
   // memory instead of registers (fewer registers, more resident CTAs)
