@@ -177,7 +177,12 @@ struct StpSmem {
 #ifndef EDG_STP_G2D_BIG
 #define EDG_STP_G2D_BIG 8
 #endif
-  static constexpr int G = DIM == 2 ? (N >= 6 ? EDG_STP_G2D_BIG : EDG_STP_G2D) : EDG_STP_G3D;
+  // 3-D n <= 5: all time nodes in one stage too (+1 % on cfg3); n = 6 keeps
+  // pairs (a single stage would need 155 KB of flux buffers per CTA)
+#ifndef EDG_STP_G3D_BIG
+#define EDG_STP_G3D_BIG 8
+#endif
+  static constexpr int G = DIM == 2 ? (N >= 6 ? EDG_STP_G2D_BIG : EDG_STP_G2D) : (N <= 5 ? EDG_STP_G3D_BIG : EDG_STP_G3D);
 #endif
   // EDG_STP_QHS: keep the Picard iterate qhat in (thread-private) shared
   // memory instead of registers (fewer registers, more resident CTAs)
