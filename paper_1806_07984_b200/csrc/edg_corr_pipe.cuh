@@ -122,6 +122,41 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
       bulk[i] = ((reinterpret_cast<uintptr_t>(srcs[i]) & 15) == 0) && ((cnt[i] * 8) % 16 == 0);
       if (bulk[i]) bulk_bytes += (unsigned)cnt[i] * 8u;
     }
+    constexpr int BLK = M * NF;
+    // uniform grids whose face blocks are 16-byte multiples (2-D p = 5 / p = 3):
+    // every copy of the group -- the contiguous blocks and the 2d neighbour
+    // face blocks -- goes through the bulk-copy engine.  The expected bytes
+    // are registered (no arrival) before any copy is issued, copies are issued
+    // by one thread per block, and thread 0 arrives afterwards.
+    if constexpr (GRID && (BLK * 8) % 16 == 0 && (TRC * 8) % 16 == 0) {
+      bool all = (reinterpret_cast<uintptr_t>(A.trace_q) & 15) == 0;
+#pragma unroll
+      for (int i = 0; i < NBK; ++i) all = all && bulk[i];
+      if (all) {
+        if (tid == 0) mbar_expect_tx(bar, bulk_bytes + (unsigned)(nc * 2 * DIM * BLK * 8));
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+          for (int i = 0; i < NBK; ++i) bulk_g2s(dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
+        }
+        double* nq = st + C::QE + (C::NB - 1) * C::TB;
+        for (int bi = tid; bi < nc * 2 * DIM; bi += THREADS) {
+          const int sl = bi / (2 * DIM), fs = bi - sl * (2 * DIM);
+          const int a = fs >> 1, s = fs & 1;
+          const unsigned cell = (unsigned)(c0 + sl);
+          const unsigned q = a == DIM - 1 ? cell : (a == DIM - 2 ? fdn.div(cell) : fdn2.div(cell));
+          const int ia = (int)(q - fdn.div(q) * (unsigned)n);
+          const int stride = a == DIM - 1 ? 1 : (a == DIM - 2 ? n : n * n);
+          int j = ia + (s ? 1 : -1);
+          if (j < 0 || j >= n) j = A.periodic ? (j < 0 ? n - 1 : 0) : -1;
+          const double* src = j >= 0 ? A.trace_q + (size_t)((int)cell + (j - ia) * stride) * TRC + (size_t)(2 * a + (1 - s)) * BLK
+                                     : A.trace_q + (size_t)cell * TRC + (size_t)fs * BLK;
+          bulk_g2s(nq + (sl * 2 * DIM + fs) * BLK, src, (unsigned)(BLK * 8), bar);
+        }
+        if (tid == 0) mbar_arrive(bar);
+        return;
+      }
+    }
     if (tid == 0) {
       mbar_arrive_expect_tx(bar, bulk_bytes);
 #pragma unroll
@@ -132,7 +167,6 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
     for (int i = 0; i < NBK; ++i)
       if (!bulk[i]) cp_block<THREADS>(dsts[i], srcs[i], cnt[i], tid);
     double* nq = st + C::QE + (C::NB - 1) * C::TB;
-    constexpr int BLK = M * NF;
     constexpr int NW = THREADS / 32;
     const int warp = tid >> 5, lane = tid & 31;
     for (int bi = warp; bi < nc * 2 * DIM; bi += NW) {

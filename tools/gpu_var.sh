@@ -9,7 +9,7 @@ for v in ${VARS:-base}; do
   for c in ${CFGS:-c02 c09 c5}; do
     case $c in
       c02) A="--cfl 0.2";; c09) A="";; c5) A="--config cfg5 --steps 20";; c3) A="--config cfg3 --steps 6 --warmup 3";;
-      c1) A="--config cfg1 --steps 17";; c4) A="--config cfg4 --steps 20";;
+      c1) A="--config cfg1 --steps 17";; c3f) A="--config cfg3 --steps 20 --warmup 3";; c4) A="--config cfg4 --steps 20";;
     esac
     EDG_LIB=$lib timeout 300 python bench.py $A $Q >> $D/${c}_$v.jsonl 2>&1
   done
