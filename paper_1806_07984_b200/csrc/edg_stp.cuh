@@ -177,10 +177,10 @@ struct StpSmem {
 #ifndef EDG_STP_G2D_BIG
 #define EDG_STP_G2D_BIG 8
 #endif
-  // 3-D n <= 5: all time nodes in one stage too (+1 % on cfg3); n = 6 keeps
-  // pairs (a single stage would need 155 KB of flux buffers per CTA)
+  // 3-D: pipelined pairs (one stage of all 5 time nodes measured +1 % over
+  // steps 4-9 of cfg3 but 31 % slower over the full 20-step bench)
 #ifndef EDG_STP_G3D_BIG
-#define EDG_STP_G3D_BIG 8
+#define EDG_STP_G3D_BIG 2
 #endif
   static constexpr int G = DIM == 2 ? (N >= 6 ? EDG_STP_G2D_BIG : EDG_STP_G2D) : (N <= 5 ? EDG_STP_G3D_BIG : EDG_STP_G3D);
 #endif
