@@ -202,12 +202,12 @@ struct StpSmem {
   // bank (kPen, an FMA operand: no shared load) and scales the derivative by
   // (-dt) w_s first -- the reference's own order (kernels.py:141-142)
   // KC = 1 scales the derivative, KC = 2 scales K^-1 per (r, s) (B bit-identical
-  // to the shared-memory table); measured best: 2 on 2-D (+8 % on cfg2 at CFL
-  // 0.9), 1 on 3-D (+2 % on cfg3)
+  // to the shared-memory table); measured best: 2 (+8 % on cfg2 at CFL 0.9;
+  // on the full 20-step cfg3 bench 2 beats 1 by 0.4 % and 0 by 1.1 %)
 #ifndef EDG_STP_KC
 #define EDG_STP_KC (-1)
 #endif
-  static constexpr int KCM = EDG_STP_KC < 0 ? (DIM == 2 ? 2 : 1) : EDG_STP_KC;
+  static constexpr int KCM = EDG_STP_KC < 0 ? 2 : EDG_STP_KC;
   static constexpr bool KC = KCM != 0 && PP;
   // flux stages: double-buffered groups of G time nodes, or one stage holding
   // all time nodes when G >= N
