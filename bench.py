@@ -265,6 +265,27 @@ def cpu_port_rate(cfg_name, cfl, seconds, cores=None, steps=1):
     return rates, cores, sample
 
 
+def cpu_batched_rate(cfg, cells=81):
+    """DoF-updates/s of the batched numpy restatement (oracle/drivers.py +
+    oracle/batched.py: one Algorithm-1 step with the cell axis vectorised) in
+    this process, on a cells^d grid of the configuration's physics (SURVEY.md
+    section 8(d) d4 asks for it beside the per-cell port, labelled)."""
+    from oracle import drivers, ops as oops
+    c = cfg.with_(cells=cells)
+    Q0 = cf.initial_dg_uniform(c)
+    pde = oops.euler(c.dim) if c.pde == "euler" else (oops.advection(c.velocity, c.dim) if c.pde == "advection"
+                                                        else oops.make_pde(c.pde, dim=c.dim))
+    basis = oops.basis_for(c.order)
+    t0 = time.perf_counter()
+    drivers.dg_uniform_step(Q0, pde, basis, cells, c.dim, c.periodic, c.cfl)
+    sec = time.perf_counter() - t0
+    dof = Q0.size
+    threads = os.environ.get("OPENBLAS_NUM_THREADS", "default")
+    return {"value": dof / sec, "unit": UNIT, "cores": 1, "kind": "port-batched",
+            "sample": f"one step of the batched numpy restatement on {cells}^{c.dim} cells of {cfg.name}'s physics, "
+                      f"one process (OPENBLAS_NUM_THREADS={threads})"}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -462,6 +483,11 @@ def run_ours(args, cfg):
         rates, cores, sample = cpu_port_rate(cfg.name, args.cfl, args.cpu_seconds, steps=1)
         cpu = {"value": rates[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
                "cpu": cpu_model()}
+        if cfg.dim == 2:
+            try:
+                cpu["batched_restatement"] = cpu_batched_rate(cfg)
+            except Exception as exc:   # reported baseline only; never fails the bench
+                cpu["batched_restatement"] = {"unavailable": repr(exc)[:200]}
     if rank == 0:
         line = {
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
