@@ -1,23 +1,26 @@
 // Space-time predictor (Picard) kernel -- replaces kernels.py:120-159.
 //
 // Mapping: one thread per spatial node, CPB cells per
-// CTA (~128-160 threads, so several CTAs -- and barrier domains -- share an
-// SM).  A thread keeps the whole time column of its node in registers
-// (qhat[n_t][m] and the next iterate acc[n_t][m]), so the K^-1 time
-// contraction is thread-local; the per-axis derivative contractions read the
-// flux of one time node from shared memory (double-buffered, one barrier per
-// time node), where all lanes on one pencil read the same word (broadcast).
+// CTA (~100-128 threads, 3 CTAs -- and barrier domains -- per SM in 2-D, 2 in
+// 3-D), persistent CTAs walking Picard-ordered work blocks with the next
+// block's initial state prefetched by cp.async.  A thread keeps the whole
+// time column of its node in registers (qhat[n_t][m] and the next iterate
+// acc[n_t][m], swapping roles every iteration), so the K^-1 time contraction
+// is thread-local (K^-1 from the constant bank); the per-axis derivative
+// contractions read the flux of a time node from shared memory.  In 2-D
+// (even n) a lane quad is a 2x2 node block and the flux buffers are
+// block-major, so each quad asks for 2 words per load (one wavefront).
 //
 // Per Picard iteration and cell, with B[r][s] = K^-1[r][s] * (-dt w_s) and
 // c = K^-1 lift (kernels.py:134-142):
 //     acc[r] = c_r q + sum_s B[r][s] sum_a (D/h_a) (x)_a F_a(qhat_s)
 // then the per-cell exit of kernels.py:143-147 (delta = max |acc - qhat| <
 // tol, NaN never below) is decided as "every |acc - qhat| < tol" by a
-// per-thread predicate and a per-cell shared flag.  Converged cells stop updating; the CTA
-// runs until its last cell stops (the solver orders cells by their previous
-// Picard count so that CTAs are homogeneous).  The epilogue
-// (kernels.py:148-157) forms q_end, q_int and the time-integrated flux,
-// stages them in shared memory and projects them onto the 2d faces.
+// per-thread predicate and a per-cell shared flag.  Converged cells stop
+// updating; the CTA runs until its last cell stops (the solver orders cells
+// by their previous Picard count so that CTAs are homogeneous).  The
+// epilogue (kernels.py:148-157) forms q_end, q_int and the time-integrated
+// flux, stages them in shared memory and projects them onto the 2d faces.
 #pragma once
 #include "edg_common.cuh"
 
