@@ -245,8 +245,36 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   const int c0 = Z4 ? (tid / (K / 2)) * K + tid % (K / 2) : tid * CPT;
   const bool ok = c0 < NC;
   const int x0 = ok ? ext_of_cell(c0) : ext_of_cell(0);
-  State me[CPT];
   double o[CPT][M];
+  // EDG_FV_JOUTER=1 (with Z4): volume-outer loop order -- one volume's state,
+  // both interface fluxes and its update are live at a time (the axis-outer
+  // order keeps both volumes' states live: spills at the 3-CTA register cap)
+#ifndef EDG_FV_JOUTER
+#define EDG_FV_JOUTER 1
+#endif
+  if constexpr (Z4 && EDG_FV_JOUTER) {
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      State mj;
+      load(x0 + j * DZ, mj);
+#pragma unroll
+      for (int k = 0; k < M; ++k) o[j][k] = mj.q[k];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const double coef = sCoef[a];
+        const int st = estride(a);
+        State nb;
+        double fl[M], fh[M];
+        load(x0 + j * DZ - st, nb);
+        iface(nb, mj, a, fl);
+        load(x0 + j * DZ + st, nb);
+        iface(mj, nb, a, fh);
+#pragma unroll
+        for (int k = 0; k < M; ++k) o[j][k] = __dsub_rn(o[j][k], __dmul_rn(coef, __dsub_rn(fh[k], fl[k])));
+      }
+    }
+  } else {
+  State me[CPT];
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
     load(x0 + j * DZ, me[j]);
@@ -284,6 +312,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
         for (int k = 0; k < M; ++k) o[j][k] = __dsub_rn(o[j][k], __dmul_rn(coef, __dsub_rn(fh[k], fl[k])));
       }
     }
+  }
   }
 
   // ---- write back, non-finite count, next-step dt candidate ----
