@@ -29,7 +29,16 @@ struct CorrPipe {
 #define EDG_CORR_PIPE_TARGET 256
 #endif
   static constexpr int CPB = NPC >= 96 ? 1 : (EDG_CORR_PIPE_TARGET / NPC > 0 ? EDG_CORR_PIPE_TARGET / NPC : 1);
-  static constexpr int THREADS = ((CPB * NPC + 31) / 32) * 32 < 64 ? 64 : ((CPB * NPC + 31) / 32) * 32;
+  // EDG_CORR_WIDE (default 1): with one cell per group and more face points
+  // than nodes (3-D p = 4: 150 > 125), the CTA is sized for the face points so
+  // that the Rusanov phase is one pass over 160 threads instead of two
+#ifndef EDG_CORR_WIDE
+#define EDG_CORR_WIDE 1
+#endif
+  static constexpr int TOTF = 2 * DIM * NF;
+  static constexpr bool WIDE = EDG_CORR_WIDE && CPB == 1 && TOTF > NPC;
+  static constexpr int WORK = WIDE ? TOTF : CPB * NPC;
+  static constexpr int THREADS = ((WORK + 31) / 32) * 32 < 64 ? 64 : ((WORK + 31) / 32) * 32;
   static constexpr int TRC = 2 * DIM * M * NF;            // trace doubles per cell (one family)
   static constexpr int QE = (CPB * M * NPC + 1) & ~1;     // stage sub-blocks, even -> 16-byte aligned
   static constexpr int TB = (CPB * TRC + 1) & ~1;
@@ -230,6 +239,7 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
 
     const int cell = g * CPB + slot;
     const bool has_cell = slot < CPB && cell < A.ncells;
+    const bool cell_ok = g * CPB < A.ncells;   // (WIDE: one cell, every thread in phase 1)
     const double* qe = cur;
     const double* tq = cur + C::QE;
     const double* tf = cur + C::QE + (GRID ? C::TB : 0);
@@ -256,12 +266,12 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
       }
     }
     // phase 1: Rusanov outcome - trace_f on the 2d faces (corrector_kernel order)
-    if (GRID && has_cell) {
-      for (int f2 = node; f2 < TOT; f2 += NPC) {
+    if (GRID && (C::WIDE ? cell_ok : has_cell)) {
+      for (int f2 = C::WIDE ? tid : node; f2 < TOT; f2 += C::WIDE ? THREADS : NPC) {
         const int fs = f2 / NF, f = f2 - fs * NF;
         const int a = fs >> 1, s = fs & 1;
         double mine[M], theirs[M], out[M];
-        const int b = slot * TRC + fs * M * NF + f;
+        const int b = (C::WIDE ? 0 : slot) * TRC + fs * M * NF + f;
 #pragma unroll
         for (int k = 0; k < M; ++k) {
           mine[k] = tq[b + k * NF];
