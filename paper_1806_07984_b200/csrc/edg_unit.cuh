@@ -208,8 +208,11 @@ int EDG_FN(_stp)(int n, const StpArgs& a, cudaStream_t st) {
 
 // uniform-grid corrector: persistent, cp.async double-buffered kernel
 // (edg_corr_pipe.cuh); EDG_CORR_PIPE=0 selects the one-CTA-per-group kernel
+// (auto choice) a mesh too small to give any persistent CTA a second group has
+// nothing to overlap: the one-CTA-per-group kernel is used instead
+constexpr int kCorrUseClassic = -1000;
 template <int N, bool GRID>
-static int launch_corr_grid_n(const CorrArgs& a, cudaStream_t st) {
+static int launch_corr_grid_n(const CorrArgs& a, cudaStream_t st, bool force = true) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
   using C = CorrPipe<KIND, DIM, N, GRID>;
   auto kern = corrector_grid_pipe_kernel<KIND, DIM, N, GRID>;
@@ -217,6 +220,7 @@ static int launch_corr_grid_n(const CorrArgs& a, cudaStream_t st) {
   const int grid_cap = persistent_grid(kern, C::THREADS, C::BYTES);
   if (grid_cap < 0) return EDG_ERR_CUDA;
   const int ngroups = (a.ncells + C::CPB - 1) / C::CPB;
+  if (!force && ngroups <= grid_cap) return kCorrUseClassic;
   const int grid = ngroups < grid_cap ? ngroups : grid_cap;
   if (grid > 0) kern<<<grid, C::THREADS, C::BYTES, st>>>(a);
   return check_launch();
@@ -234,7 +238,10 @@ static int launch_corr_n(bool fused, const CorrArgs& a, cudaStream_t st) {
     const char* v = getenv("EDG_CORR_PIPE");
     return v ? (v[0] != '0' ? 1 : 0) : -1;
   }();
-  if (pipe != 0 && fused && a.grid_n > 0 && a.edges_per_cell == 0) return launch_corr_grid_n<N, true>(a, st);
+  if (pipe != 0 && fused && a.grid_n > 0 && a.edges_per_cell == 0) {
+    const int r = launch_corr_grid_n<N, true>(a, st, pipe == 1);
+    if (r != kCorrUseClassic) return r;
+  }
   if (pipe == 1 && !fused) return launch_corr_grid_n<N, false>(a, st);
   using Cf = CorrCfg<DIM, N>;
   const size_t smem = CorrSmem<KIND, DIM, N>::BYTES;

@@ -6,8 +6,8 @@ subprocess:
   EDG_STP_PAIR=1  node-pair / time-split 2-D STP (edg_stp_pair.cuh): the cfg2
                   9x9 reference trajectory (CFL 0.2) within 1e-10 and
                   identical Picard counts;
-* EDG_CORR_PIPE=0 one-CTA-per-group corrector instead of the pipelined one
-                  on 2-D and 3-D grids, and EDG_CORR_PIPE=1 the pipelined one
+* EDG_CORR_PIPE=0 one-CTA-per-group corrector against the pipelined one
+                  (EDG_CORR_PIPE=1) on 2-D and 3-D grids, and EDG_CORR_PIPE=1 the pipelined one
                   on the adaptive cfg5 mesh: bitwise equal to the defaults;
 * EDG_FV_PIPE=1   persistent FV grid kernel: bitwise equal (16^3 volumes, 5 steps).
 """
@@ -90,7 +90,10 @@ def test_pencil_stp_vs_reference(tmp_path):
 
 @pytest.mark.parametrize("tag,env", [("cfg2s", {"EDG_CORR_PIPE": "0"}), ("cfg3w", {"EDG_CORR_PIPE": "0"})])
 def test_corrector_variants_bitwise(tmp_path, tag, env):
-    a = _run(tmp_path, {}, "dg", tag)
+    # the small test grids give every persistent CTA at most one group, so the
+    # automatic choice would take the one-CTA-per-group kernel: force the
+    # pipelined one (EDG_CORR_PIPE=1) against it
+    a = _run(tmp_path, {"EDG_CORR_PIPE": "1"}, "dg", tag)
     b = _run(tmp_path, env, "dg", tag)
     assert np.array_equal(a["q"], b["q"])
     assert np.array_equal(a["dt"], b["dt"])
