@@ -355,6 +355,26 @@ stp_picard_kernel(const StpArgs A) {
     else return (a == DIM - 1 || (Sm::T0 && a == 0)) ? j : j * st;
   };
   unsigned its_sum = 0u;
+#ifndef EDG_STP_CLIFT
+#define EDG_STP_CLIFT 1
+#endif
+#ifndef EDG_STP_DRH
+#define EDG_STP_DRH 1
+#endif
+  // derivative rows of this node, scaled by 1/h_a: once per CTA on uniform
+  // meshes (shared edges), per work block when the edges are per cell
+  double Dr[DIM][N];
+  auto load_dr = [&](int cell) {
+    const double* e = A.edges + (A.edges_per_cell ? (size_t)cell * DIM : 0);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const double ih = 1.0 / e[a];
+#pragma unroll
+      for (int j = 0; j < N; ++j) Dr[a][j] = sD[ix[a] * N + j] * ih;
+    }
+  };
+  constexpr bool kDrOnce = EDG_STP_DRH != 0 && DIM == 3;   // (2-D n = 6: spills at the 3-CTA cap)
+  if (kDrOnce && !A.edges_per_cell) load_dr(0);
 
   for (int gi = 0; blk < nblocks; blk += gridDim.x, ++gi) {
   const int item = blk * CPB + slot;
@@ -363,17 +383,7 @@ stp_picard_kernel(const StpArgs A) {
   if (blk + (int)gridDim.x < nblocks) prefetch_q(blk + gridDim.x, (gi + 1) & 1);
   cp_async_commit();
   if (tid < 2 * CPB) sFlag[tid] = 0;
-  // derivative rows of this node, scaled by 1/h_a
-  double Dr[DIM][N];
-  {
-    const double* e = A.edges + (A.edges_per_cell ? (size_t)cell * DIM : 0);
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-      const double ih = 1.0 / e[a];
-#pragma unroll
-      for (int j = 0; j < N; ++j) Dr[a][j] = sD[ix[a] * N + j] * ih;
-    }
-  }
+  if (!kDrOnce || A.edges_per_cell) load_dr(cell);
   cp_async_wait1();   // this block's initial state (own node) has landed
 
   // the initial state is re-read every iteration (c_r q): private copy in
@@ -517,7 +527,11 @@ stp_picard_kernel(const StpArgs A) {
           for (int k = 0; k < M; ++k) {
             const double q0 = q0s[k * NPC];
 #pragma unroll
-            for (int r = 0; r < N; ++r) qn[r][k] = sC[r] * q0;
+            for (int r = 0; r < N; ++r) {
+              // K^-1 lift: a uniform constant-bank operand when the table is there
+              const double c = (Sm::KC && EDG_STP_CLIFT && DIM == 3) ? kPen[pen_off(N) + EDG_BASIS_KLIFT(N) + r] : sC[r];
+              qn[r][k] = c * q0;
+            }
           }
 #pragma unroll
           for (int g = 0; g < G; ++g)
