@@ -358,17 +358,25 @@ stp_picard_kernel(const StpArgs A) {
 #ifndef EDG_STP_CLIFT
 #define EDG_STP_CLIFT 1
 #endif
+#ifndef EDG_STP_IHS
+#define EDG_STP_IHS 1
+#endif
 #ifndef EDG_STP_DRH
 #define EDG_STP_DRH 1
 #endif
   // derivative rows of this node, scaled by 1/h_a: once per CTA on uniform
   // meshes (shared edges), per work block when the edges are per cell
   double Dr[DIM][N];
+  // uniform meshes: 1/h_a once per CTA in shared memory (the per-block
+  // rebuild of the 2-D rows then costs no division and no global load)
+  __shared__ double sIh[DIM];
+  if (!A.edges_per_cell && tid < DIM) sIh[tid] = 1.0 / A.edges[tid];
+  __syncthreads();
   auto load_dr = [&](int cell) {
     const double* e = A.edges + (A.edges_per_cell ? (size_t)cell * DIM : 0);
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-      const double ih = 1.0 / e[a];
+      const double ih = (EDG_STP_IHS && !A.edges_per_cell) ? sIh[a] : 1.0 / e[a];
 #pragma unroll
       for (int j = 0; j < N; ++j) Dr[a][j] = sD[ix[a] * N + j] * ih;
     }
