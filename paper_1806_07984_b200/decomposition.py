@@ -1,0 +1,204 @@
+"""Domain decomposition host logic ("next").
+
+North_star runs one GPU with no sharding, so this module is the host half of
+the multi-GPU step only: the SFC split of the cells, the rank-boundary face
+lists both sides derive identically, the skeleton rule widened by rank
+boundaries, and the per-step exchange plumbing (face traces to each
+neighbour rank, dt as a global MIN) over `torch.distributed`.
+
+Reference anchors:
+  * `decomp.rank_of(key)` / `decomp.nranks` / `decomp.version` as consumed by
+    `mesh.py:537-567` (secondary_order) and `mesh.py:599-610`;
+  * `classify_cell(mesh, node, decomp)` `mesh.py:585-596` -- a cell that
+    touches a rank boundary is skeleton;
+  * `boundary_face_order(mesh, decomp, rank_pair)` `mesh.py:613-628` -- the
+    shared faces of a rank pair, the same list from either rank, ConfigError
+    on an unknown pair;
+  * SPEC.md:425-508 (rank-sim): `decompose(mesh, R)` splits the SFC order
+    into R contiguous segments whose cell counts differ by at most one,
+    ConfigError for R outside [1, ncells].
+
+B200 design choice: the reference sends one message per face (SPEC.md
+rank-sim "deliberately per-face"); over NVLink a message costs launch
+latency, not bandwidth, so `exchange_traces` sends ONE contiguous buffer per
+neighbour rank per step, laid out in boundary_face_order, so the receiver's
+rows line up with its own boundary-face list without an index map.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ConfigError
+from .mesh import AdaptiveMesh, CartesianMesh
+
+
+def _morton3_key(idx, depth):
+    """Morton order over the 3-ary index space (SPEC.md rank-sim design
+    decisions): the level-l digit of every axis, coarsest level first."""
+    return tuple(tuple((i // 3 ** (depth - l)) % 3 for i in idx) for l in range(1, depth + 1))
+
+
+def sfc_order(mesh):
+    """Cell indices of `mesh` in space-filling-curve order."""
+    if isinstance(mesh, AdaptiveMesh):
+        return np.arange(mesh.ncells, dtype=np.int64)   # cells are stored in SFC order
+    if isinstance(mesh, CartesianMesh):
+        depth = 1
+        while 3 ** depth < mesh.N:
+            depth += 1
+        keys = [_morton3_key(tuple(int(v) for v in row), depth) for row in mesh.index]
+        return np.array(sorted(range(mesh.ncells), key=keys.__getitem__), dtype=np.int64)
+    raise ConfigError(f"unsupported mesh type {type(mesh).__name__}")
+
+
+def interior_faces(mesh):
+    """(F, 2) int64 owner cells (lo, hi) of every leaf face between two
+    distinct real cells, in the mesh's canonical face order, plus each face's
+    sort key (axis, level, position) -- the reference FaceRecord.key,
+    `mesh.py:92-94`.  Domain-boundary faces are excluded; a hanging child
+    face lists its coarse owner on the virtual side."""
+    if isinstance(mesh, AdaptiveMesh):
+        keep = (mesh.face_kind != 2).all(axis=1) & (mesh.face_cell[:, 0] != mesh.face_cell[:, 1])
+        keys = [(k[1], k[2], k[3]) for k, ok in zip(mesh._leaf_keys, keep) if ok]
+        return mesh.face_cell[keep].astype(np.int64), keys
+    if isinstance(mesh, CartesianMesh):
+        out, keys = [], []
+        for a in range(mesh.dim):
+            hi = mesh.nbr[:, 2 * a + 1].astype(np.int64)
+            lo = np.arange(mesh.ncells, dtype=np.int64)
+            ok = (hi >= 0) & (hi != lo)
+            out.append(np.stack([lo[ok], hi[ok]], axis=1))
+            keys.extend((a, 0, int(c)) for c in lo[ok])
+        return np.concatenate(out, axis=0), keys
+    raise ConfigError(f"unsupported mesh type {type(mesh).__name__}")
+
+
+@dataclass
+class DomainDecomposition:
+    """Cell -> rank map from contiguous cuts of the SFC order."""
+    nranks: int
+    cell_rank: np.ndarray          # (ncells,) int32
+    version: int = 0
+
+    def rank_of(self, cell):
+        return int(self.cell_rank[cell])
+
+    def cells_of(self, rank):
+        return np.nonzero(self.cell_rank == rank)[0].astype(np.int32)
+
+
+def decompose(mesh, nranks: int) -> DomainDecomposition:
+    """SPEC.md rank-sim `decompose`: R contiguous SFC segments, sizes differ by <= 1
+    (the first ncells % R segments hold one extra cell)."""
+    n = mesh.ncells
+    if not (1 <= nranks <= n):
+        raise ConfigError(f"rank count {nranks} outside [1, {n}]")
+    order = sfc_order(mesh)
+    base, extra = divmod(n, nranks)
+    sizes = np.full(nranks, base, dtype=np.int64)
+    sizes[:extra] += 1
+    seg = np.repeat(np.arange(nranks, dtype=np.int32), sizes)
+    cell_rank = np.empty(n, dtype=np.int32)
+    cell_rank[order] = seg
+    return DomainDecomposition(nranks, cell_rank, version=getattr(mesh, "version", 0))
+
+
+def boundary_face_order(mesh, decomp: DomainDecomposition, rank_pair):
+    """Indices into `interior_faces(mesh)` of the faces shared by the two
+    ranks, identical from either rank, in the reference's secondary-sweep
+    order (`mesh.py:552-564`, `mesh.py:613-628`): a face is emitted after the
+    later of its two owners in SFC order, ties broken by face key."""
+    r1, r2 = rank_pair
+    if not (0 <= r1 < decomp.nranks and 0 <= r2 < decomp.nranks):
+        raise ConfigError(f"unknown rank pair {rank_pair}")
+    if r1 == r2:
+        return np.zeros(0, dtype=np.int64)
+    faces, keys = interior_faces(mesh)
+    ra, rb = decomp.cell_rank[faces[:, 0]], decomp.cell_rank[faces[:, 1]]
+    sel = np.nonzero(((ra == r1) & (rb == r2)) | ((ra == r2) & (rb == r1)))[0]
+    pos = np.empty(mesh.ncells, dtype=np.int64)
+    pos[sfc_order(mesh)] = np.arange(mesh.ncells)
+    later = np.maximum(pos[faces[:, 0]], pos[faces[:, 1]])
+    return np.array(sorted(sel.tolist(), key=lambda f: (int(later[f]), keys[f])), dtype=np.int64)
+
+
+def skeleton_mask(mesh, decomp: DomainDecomposition | None):
+    """`classify_cell` with a decomposition (`mesh.py:585-596`): skeleton iff
+    one of the cell's sides is a parent face (the coarse side of a
+    resolution transition) or a face below it joins cells on two ranks.
+    (Config 5's schedule rule, `AdaptiveMesh.skeleton_mask`, also marks the
+    fine side and the synthetic cut.)"""
+    if isinstance(mesh, AdaptiveMesh):
+        mask = (mesh.side_face >= mesh.nleaf).any(axis=1)
+    else:
+        mask = np.zeros(mesh.ncells, dtype=bool)
+    if decomp is not None:
+        faces, _ = interior_faces(mesh)
+        cross = decomp.cell_rank[faces[:, 0]] != decomp.cell_rank[faces[:, 1]]
+        mask[faces[cross].ravel()] = True
+    return mask
+
+
+@dataclass
+class ExchangePlan:
+    """Per-rank view: for each neighbour rank, the shared faces (indices into
+    interior_faces) and, per face, this rank's local owner cell and the
+    side (0 = lo, 1 = hi) that cell occupies."""
+    rank: int
+    peers: list
+    faces: dict          # peer -> (k,) int64 face indices in boundary_face_order
+    local_cell: dict     # peer -> (k,) int64 cell owned by `rank`
+    local_side: dict     # peer -> (k,) int8
+
+
+def exchange_plan(mesh, decomp: DomainDecomposition, rank: int) -> ExchangePlan:
+    faces, _ = interior_faces(mesh)
+    peers, fmap, cmap, smap = [], {}, {}, {}
+    for q in range(decomp.nranks):
+        if q == rank:
+            continue
+        f = boundary_face_order(mesh, decomp, (rank, q))
+        if f.size == 0:
+            continue
+        lo_mine = decomp.cell_rank[faces[f, 0]] == rank
+        peers.append(q)
+        fmap[q] = f
+        cmap[q] = np.where(lo_mine, faces[f, 0], faces[f, 1])
+        smap[q] = np.where(lo_mine, 0, 1).astype(np.int8)
+    return ExchangePlan(rank, peers, fmap, cmap, smap)
+
+
+def exchange_traces(dist, plan: ExchangePlan, send: dict):
+    """Send `send[peer]` (rows in the peer's boundary_face_order) to every
+    peer and return {peer: received rows}.  One message per neighbour per
+    step; tensors may live on the GPU (NCCL) or the CPU (gloo)."""
+    import torch
+    reqs, recv = [], {}
+    for q in plan.peers:
+        buf = send[q]
+        if buf.shape[0] != plan.faces[q].shape[0]:
+            raise ConfigError(f"payload for rank {q} has {buf.shape[0]} rows, expected {plan.faces[q].shape[0]}")
+        recv[q] = torch.empty_like(buf)
+    for q in plan.peers:
+        # lower rank sends first so the pairwise order never deadlocks on blocking backends
+        if plan.rank < q:
+            reqs.append(dist.isend(send[q].contiguous(), q))
+            reqs.append(dist.irecv(recv[q], q))
+        else:
+            reqs.append(dist.irecv(recv[q], q))
+            reqs.append(dist.isend(send[q].contiguous(), q))
+    for r in reqs:
+        r.wait()
+    return recv
+
+
+def global_dt(dist, local_dt):
+    """Admissible dt of the whole domain: all-reduce MIN of the per-rank dt
+    (the device reduction `edg_dt_finalize` yields the per-rank value)."""
+    import torch
+    t = local_dt if isinstance(local_dt, torch.Tensor) else torch.tensor([float(local_dt)], dtype=torch.float64)
+    t = t.reshape(1).clone()
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return t

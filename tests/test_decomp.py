@@ -1,0 +1,121 @@
+"""Row f3 host logic: SFC decomposition, rank-boundary face order, skeleton
+rule with ranks (pinned to the reference mesh through tests/golden/decomp.json,
+made by tests/golden/make_golden_decomp.py), and the per-neighbour trace
+exchange + dt all-reduce over gloo with world size 2."""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1806_07984_b200.decomposition import (boundary_face_order, decompose, exchange_plan, interior_faces,
+                                                 skeleton_mask)
+from paper_1806_07984_b200.errors import ConfigError
+from paper_1806_07984_b200.mesh import AdaptiveMesh, CartesianMesh
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "decomp.json")))
+
+
+def _key(k):
+    return tuple(tuple(x) if isinstance(x, list) else x for x in k)
+
+
+@pytest.mark.parametrize("name", ["uniform9", "refined"])
+def test_against_reference_mesh(name):
+    G = GOLDEN[name]
+    cells = [_key(c) for c in G["cells"]]
+    mesh = AdaptiveMesh(cells, 2, True)
+    assert mesh.cells == cells                      # same SFC order as the reference
+    faces, fkeys = interior_faces(mesh)
+    for case in G["cases"]:
+        R = case["R"]
+        dec = decompose(mesh, R)
+        sizes = np.bincount(dec.cell_rank, minlength=R)
+        assert sizes.max() - sizes.min() <= 1
+        for pair, want in case["pairs"].items():
+            r1, r2 = map(int, pair.split(","))
+            got = boundary_face_order(mesh, dec, (r1, r2))
+            assert list(got) == list(boundary_face_order(mesh, dec, (r2, r1)))
+            got_t = [(cells[faces[f, 0]], cells[faces[f, 1]], fkeys[f]) for f in got]
+            want_t = [(_key(lo), _key(hi), _key(fk)) for lo, hi, fk in want]
+            assert got_t == want_t
+        skel = {cells[i] for i in np.nonzero(skeleton_mask(mesh, dec))[0]}
+        assert skel == {_key(c) for c in case["skeleton"]}
+
+
+def test_decompose_examples():
+    m81 = CartesianMesh(9, 2, True)
+    d1 = decompose(m81, 1)
+    assert (d1.cell_rank == 0).all()
+    d2 = decompose(m81, 2)
+    assert sorted(np.bincount(d2.cell_rank).tolist()) == [40, 41]
+    m9 = CartesianMesh(3, 2, True)
+    d3 = decompose(m9, 3)
+    assert np.bincount(d3.cell_rank).tolist() == [3, 3, 3]
+    faces, _ = interior_faces(m9)
+    brute = {i for i, (a, b) in enumerate(faces) if d3.cell_rank[a] != d3.cell_rank[b]}
+    got = set()
+    for r1 in range(3):
+        for r2 in range(r1 + 1, 3):
+            got |= set(boundary_face_order(m9, d3, (r1, r2)).tolist())
+    assert got == brute
+    assert boundary_face_order(m81, d1, (0, 0)).size == 0
+    with pytest.raises(ConfigError):
+        decompose(m9, 0)
+    with pytest.raises(ConfigError):
+        decompose(m9, 10)
+    with pytest.raises(ConfigError):
+        boundary_face_order(m9, d3, (0, 3))
+
+
+def _payload(plan, peer, nvar=4):
+    import torch
+    # row = (face index, local cell, side) -- what the sender holds for that face
+    f = torch.from_numpy(plan.faces[peer]).double()
+    c = torch.from_numpy(plan.local_cell[peer]).double()
+    s = torch.from_numpy(plan.local_side[peer].astype(np.float64))
+    return torch.stack([f * 1000 + c + 0.5 * s + v for v in range(nvar)], dim=1)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_1806_07984_b200.decomposition import exchange_traces, global_dt
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mesh = AdaptiveMesh([(2, (i, j)) for i in range(9) for j in range(9)], 2, True)
+    dec = decompose(mesh, world)
+    plan = exchange_plan(mesh, dec, rank)
+    recv = exchange_traces(dist, plan, {p: _payload(plan, p) for p in plan.peers})
+    ok = True
+    for p in plan.peers:
+        peer_plan = exchange_plan(mesh, dec, p)
+        ok &= bool(np.array_equal(peer_plan.faces[rank], plan.faces[p]))
+        ok &= bool(torch.equal(recv[p], _payload(peer_plan, rank)))
+    dt = global_dt(dist, 0.1 * (rank + 1))
+    q.put((rank, ok, len(plan.peers), float(dt)))
+    dist.destroy_process_group()
+
+
+def test_exchange_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get() for _ in range(2))
+    assert [r[1] for r in res] == [True, True]
+    assert [r[2] for r in res] == [1, 1]
+    assert [r[3] for r in res] == [0.1, 0.1]
