@@ -233,6 +233,19 @@ int edg_stream_priority_range(int32_t* least, int32_t* greatest);
 /* Last CUDA error string of this thread (static storage). */
 const char* edg_last_error(void);
 
+/* ---- rank-boundary trace exchange (host half in
+ * decomposition.py; replaces the per-face send_face / receive_face payloads of
+ * SPEC.md:425-508 and boundary_face_order mesh.py:613-628) ----------------
+ * edg_pack_face_traces: out[j][0] = trace_q[cell[j]][side[j]],
+ *   out[j][1] = trace_f[cell[j]][side[j]] (row_len = m*n^(d-1) doubles each;
+ *   traces (C, nsides, row_len)); out is the send buffer (nfaces, 2, row_len).
+ * edg_unpack_face_traces: ghost[slot[j]] = in[j] (ghost (G, 2, row_len)). */
+int edg_pack_face_traces(int32_t nsides, int32_t row_len, int32_t nfaces, const int32_t* cell_dev,
+                         const int8_t* side_dev, const double* trace_q_dev, const double* trace_f_dev,
+                         double* out_dev, void* stream);
+int edg_unpack_face_traces(int32_t row_len, int32_t nfaces, const int32_t* slot_dev, const double* in_dev,
+                           double* ghost_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

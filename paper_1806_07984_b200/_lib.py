@@ -59,6 +59,8 @@ SIGNATURES = {
     "edg_gradient_indicator": (C.c_int, [I32, I32, I32, P, I32, P, P, D, D, I32, I32, P, P, P]),
     "edg_interpolate_volume": (C.c_int, [I32, I32, I32, P, I32, P, P, P, P, P]),
     "edg_restrict_volume": (C.c_int, [I32, I32, I32, P, I32, P, P, P]),
+    "edg_pack_face_traces": (C.c_int, [I32, I32, I32, P, P, P, P, P, P]),
+    "edg_unpack_face_traces": (C.c_int, [I32, I32, P, P, P, P]),
 }
 
 _LIB = None

@@ -151,11 +151,13 @@ class ExchangePlan:
     faces: dict          # peer -> (k,) int64 face indices in boundary_face_order
     local_cell: dict     # peer -> (k,) int64 cell owned by `rank`
     local_side: dict     # peer -> (k,) int8
+    local_fs: dict       # peer -> (k,) int8: the local cell's side slot 2*axis + s of the face
 
 
 def exchange_plan(mesh, decomp: DomainDecomposition, rank: int) -> ExchangePlan:
-    faces, _ = interior_faces(mesh)
-    peers, fmap, cmap, smap = [], {}, {}, {}
+    faces, keys = interior_faces(mesh)
+    axis = np.array([k[0] for k in keys], dtype=np.int64)
+    peers, fmap, cmap, smap, fsmap = [], {}, {}, {}, {}
     for q in range(decomp.nranks):
         if q == rank:
             continue
@@ -167,7 +169,38 @@ def exchange_plan(mesh, decomp: DomainDecomposition, rank: int) -> ExchangePlan:
         fmap[q] = f
         cmap[q] = np.where(lo_mine, faces[f, 0], faces[f, 1])
         smap[q] = np.where(lo_mine, 0, 1).astype(np.int8)
-    return ExchangePlan(rank, peers, fmap, cmap, smap)
+        # the lo owner sees the face on its upper side (s = 1), the hi owner on its lower side
+        fsmap[q] = (2 * axis[f] + np.where(lo_mine, 1, 0)).astype(np.int8)
+    return ExchangePlan(rank, peers, fmap, cmap, smap, fsmap)
+
+
+def pack_boundary_traces(plan: ExchangePlan, peer: int, trace_q, trace_f):
+    """Send buffer (k, 2, m*n^(d-1)) for `peer` gathered on the device by
+    `edg_pack_face_traces` from the STP traces (C, 2d, m, n^(d-1))."""
+    import torch
+    from . import _lib
+    from .kernels import _stream
+    C_, nsides = trace_q.shape[0], trace_q.shape[1]
+    row_len = trace_q[0, 0].numel()
+    dev = trace_q.device
+    cell = torch.from_numpy(plan.local_cell[peer].astype(np.int32)).to(dev)
+    side = torch.from_numpy(plan.local_fs[peer]).to(dev)
+    out = torch.empty((cell.numel(), 2, row_len), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().edg_pack_face_traces(nsides, row_len, cell.numel(), _lib.ptr(cell), _lib.ptr(side),
+                                                _lib.ptr(trace_q), _lib.ptr(trace_f), _lib.ptr(out),
+                                                _stream()), "pack face traces")
+    return out
+
+
+def unpack_boundary_traces(recv, slots, ghost):
+    """Scatter received rows (k, 2, L) into ghost[slots] (G, 2, L) on the device."""
+    import torch
+    from . import _lib
+    from .kernels import _stream
+    slot = torch.as_tensor(np.asarray(slots, dtype=np.int32)).to(ghost.device)
+    _lib.check(_lib.load().edg_unpack_face_traces(recv.shape[-1], recv.shape[0], _lib.ptr(slot), _lib.ptr(recv),
+                                                  _lib.ptr(ghost), _stream()), "unpack face traces")
+    return ghost
 
 
 def exchange_traces(dist, plan: ExchangePlan, send: dict):

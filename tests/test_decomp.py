@@ -119,3 +119,41 @@ def test_exchange_gloo_world2():
     assert [r[1] for r in res] == [True, True]
     assert [r[2] for r in res] == [1, 1]
     assert [r[3] for r in res] == [0.1, 0.1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,m,n", [(2, 4, 4), (3, 5, 5)])
+def test_gpu_pack_unpack_bit_exact(dim, m, n):
+    """edg_pack_face_traces / edg_unpack_face_traces against plain indexing
+    (a copy: bit-exact), on the 3-rank exchange plan of a uniform mesh."""
+    import torch
+    from paper_1806_07984_b200.decomposition import pack_boundary_traces, unpack_boundary_traces
+    mesh = CartesianMesh(9 if dim == 2 else 6, dim, True)
+    dec = decompose(mesh, 3)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    shape = (mesh.ncells, 2 * dim, m, n ** (dim - 1))
+    tq = torch.rand(shape, dtype=torch.float64, device="cuda", generator=g)
+    tf = torch.rand(shape, dtype=torch.float64, device="cuda", generator=g)
+    for rank in range(3):
+        plan = exchange_plan(mesh, dec, rank)
+        assert plan.peers
+        for p in plan.peers:
+            c = torch.from_numpy(plan.local_cell[p]).cuda()
+            s = torch.from_numpy(plan.local_fs[p].astype(np.int64)).cuda()
+            want = torch.stack([tq[c, s].flatten(1), tf[c, s].flatten(1)], dim=1)
+            got = pack_boundary_traces(plan, p, tq, tf)
+            torch.cuda.synchronize()
+            assert torch.equal(got, want)
+            k = got.shape[0]
+            slots = np.random.default_rng(rank).permutation(k + 3)[:k]
+            ghost = torch.zeros((k + 3, 2, got.shape[-1]), dtype=torch.float64, device="cuda")
+            unpack_boundary_traces(got, slots, ghost)
+            torch.cuda.synchronize()
+            assert torch.equal(ghost[torch.from_numpy(slots.astype(np.int64)).cuda()], got)
+    # the face side each rank packs is the side that touches the peer cell
+    plan = exchange_plan(mesh, dec, 0)
+    faces, keys = interior_faces(mesh)
+    for p in plan.peers:
+        for f, c, fs in zip(plan.faces[p], plan.local_cell[p], plan.local_fs[p]):
+            other = faces[f, 1] if faces[f, 0] == c else faces[f, 0]
+            assert mesh.nbr[c, fs] == other
