@@ -628,38 +628,32 @@ int edg_restrict_volume(int32_t dim, int32_t m, int32_t order, const double* bas
 // ---- rank-boundary trace exchange buffers ----
 // One send buffer per neighbour rank: row j = [trace_q | trace_f] of the
 // local owner's side fs[j] of boundary face j, rows in boundary_face_order.
-// Grid-stride copy: consecutive threads walk one contiguous row_len run, so
+// Row-per-CTA copy: the threads of a CTA walk one contiguous row_len run, so
 // loads and stores coalesce; the work is a few KB per face, HBM/latency bound.
 namespace edg {
 __global__ void pack_face_traces_kernel(int nsides, int row_len, int nfaces, const int32_t* __restrict__ cell,
                                         const int8_t* __restrict__ side, const double* __restrict__ tq,
                                         const double* __restrict__ tf, double* __restrict__ out) {
-  const long long total = 2LL * nfaces * row_len;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long row = i / row_len;
-    const int e = (int)(i - row * row_len);
-    const int j = (int)(row >> 1);
-    const double* src = (row & 1) ? tf : tq;
-    out[i] = __ldg(src + ((long long)cell[j] * nsides + side[j]) * row_len + e);
+  // one CTA per (face, q|f) row at a time: no per-element index division
+  for (int row = blockIdx.x; row < 2 * nfaces; row += gridDim.x) {
+    const int j = row >> 1;
+    const double* src = ((row & 1) ? tf : tq) + ((long long)__ldg(cell + j) * nsides + __ldg(side + j)) * row_len;
+    double* dst = out + (long long)row * row_len;
+    for (int e = threadIdx.x; e < row_len; e += blockDim.x) dst[e] = __ldg(src + e);
   }
 }
 
 __global__ void unpack_face_traces_kernel(int row_len, int nfaces, const int32_t* __restrict__ slot,
                                           const double* __restrict__ in, double* __restrict__ ghost) {
-  const long long total = 2LL * nfaces * row_len;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long row = i / row_len;
-    const int e = (int)(i - row * row_len);
-    const int j = (int)(row >> 1);
-    ghost[((long long)slot[j] * 2 + (row & 1)) * row_len + e] = in[i];
+  for (int row = blockIdx.x; row < 2 * nfaces; row += gridDim.x) {
+    const double* src = in + (long long)row * row_len;
+    double* dst = ghost + ((long long)__ldg(slot + (row >> 1)) * 2 + (row & 1)) * row_len;
+    for (int e = threadIdx.x; e < row_len; e += blockDim.x) dst[e] = __ldg(src + e);
   }
 }
 
-static unsigned copy_blocks(long long total) {
-  const long long b = (total + 255) / 256;
-  return (unsigned)(b < 148LL * 16 ? (b > 0 ? b : 1) : 148LL * 16);
+static unsigned copy_blocks(int rows) {
+  return (unsigned)(rows < 148 * 16 ? rows : 148 * 16);   // 16 CTAs of 128 threads per SM
 }
 }  // namespace edg
 
@@ -670,8 +664,7 @@ int edg_pack_face_traces(int32_t nsides, int32_t row_len, int32_t nfaces, const 
                          double* out_dev, void* stream) {
   if (nsides < 1 || row_len < 1 || nfaces < 0) return fail(EDG_ERR_CONFIG, "bad pack shape");
   if (nfaces == 0) return EDG_OK;
-  const long long total = 2LL * nfaces * row_len;
-  pack_face_traces_kernel<<<copy_blocks(total), 256, 0, (cudaStream_t)stream>>>(
+  pack_face_traces_kernel<<<copy_blocks(2 * nfaces), 128, 0, (cudaStream_t)stream>>>(
       nsides, row_len, nfaces, cell_dev, side_dev, trace_q_dev, trace_f_dev, out_dev);
   return cuda_status(check_launch());
 }
@@ -680,9 +673,8 @@ int edg_unpack_face_traces(int32_t row_len, int32_t nfaces, const int32_t* slot_
                            double* ghost_dev, void* stream) {
   if (row_len < 1 || nfaces < 0) return fail(EDG_ERR_CONFIG, "bad unpack shape");
   if (nfaces == 0) return EDG_OK;
-  const long long total = 2LL * nfaces * row_len;
-  unpack_face_traces_kernel<<<copy_blocks(total), 256, 0, (cudaStream_t)stream>>>(row_len, nfaces, slot_dev,
-                                                                                   in_dev, ghost_dev);
+  unpack_face_traces_kernel<<<copy_blocks(2 * nfaces), 128, 0, (cudaStream_t)stream>>>(row_len, nfaces, slot_dev,
+                                                                                         in_dev, ghost_dev);
   return cuda_status(check_launch());
 }
 

@@ -26,7 +26,7 @@ rows line up with its own boundary-face list without an index map.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -152,6 +152,7 @@ class ExchangePlan:
     local_cell: dict     # peer -> (k,) int64 cell owned by `rank`
     local_side: dict     # peer -> (k,) int8
     local_fs: dict       # peer -> (k,) int8: the local cell's side slot 2*axis + s of the face
+    device_index: dict = field(default_factory=dict)   # (peer, device) -> (cell int32, fs int8) on the device
 
 
 def exchange_plan(mesh, decomp: DomainDecomposition, rank: int) -> ExchangePlan:
@@ -183,8 +184,11 @@ def pack_boundary_traces(plan: ExchangePlan, peer: int, trace_q, trace_f):
     C_, nsides = trace_q.shape[0], trace_q.shape[1]
     row_len = trace_q[0, 0].numel()
     dev = trace_q.device
-    cell = torch.from_numpy(plan.local_cell[peer].astype(np.int32)).to(dev)
-    side = torch.from_numpy(plan.local_fs[peer]).to(dev)
+    key = (peer, str(dev))
+    if key not in plan.device_index:     # uploaded once per plan, not per step
+        plan.device_index[key] = (torch.from_numpy(plan.local_cell[peer].astype(np.int32)).to(dev),
+                                  torch.from_numpy(plan.local_fs[peer]).to(dev))
+    cell, side = plan.device_index[key]
     out = torch.empty((cell.numel(), 2, row_len), dtype=torch.float64, device=dev)
     _lib.check(_lib.load().edg_pack_face_traces(nsides, row_len, cell.numel(), _lib.ptr(cell), _lib.ptr(side),
                                                 _lib.ptr(trace_q), _lib.ptr(trace_f), _lib.ptr(out),
@@ -193,11 +197,15 @@ def pack_boundary_traces(plan: ExchangePlan, peer: int, trace_q, trace_f):
 
 
 def unpack_boundary_traces(recv, slots, ghost):
-    """Scatter received rows (k, 2, L) into ghost[slots] (G, 2, L) on the device."""
+    """Scatter received rows (k, 2, L) into ghost[slots] (G, 2, L) on the device
+    (`slots`: host ints, or a resident int32 device tensor)."""
     import torch
     from . import _lib
     from .kernels import _stream
-    slot = torch.as_tensor(np.asarray(slots, dtype=np.int32)).to(ghost.device)
+    if isinstance(slots, torch.Tensor) and slots.dtype == torch.int32 and slots.device == ghost.device:
+        slot = slots                     # already resident: no per-step upload
+    else:
+        slot = torch.as_tensor(np.asarray(slots, dtype=np.int32)).to(ghost.device)
     _lib.check(_lib.load().edg_unpack_face_traces(recv.shape[-1], recv.shape[0], _lib.ptr(slot), _lib.ptr(recv),
                                                   _lib.ptr(ghost), _stream()), "unpack face traces")
     return ghost
