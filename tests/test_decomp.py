@@ -157,3 +157,61 @@ def test_gpu_pack_unpack_bit_exact(dim, m, n):
         for f, c, fs in zip(plan.faces[p], plan.local_cell[p], plan.local_fs[p]):
             other = faces[f, 1] if faces[f, 0] == c else faces[f, 0]
             assert mesh.nbr[c, fs] == other
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("R", [2, 3])
+def test_gpu_redundant_riemann_agreement(R):
+    """SPEC.md rank-sim invariants on the device path: after the predictor,
+    packing each rank's own traces and swapping the buffers, the Rusanov
+    outcome each rank computes for a shared face is bitwise equal to its
+    peer's and to the single-domain outcome (rank-count transparency at the
+    face level)."""
+    import torch
+    import paper_1806_07984_b200 as edg
+    from paper_1806_07984_b200.decomposition import pack_boundary_traces
+    mesh = CartesianMesh(9, 2, True)
+    pde, p = edg.pde.euler(2), 3
+    b = edg.basis.get_basis(p)
+    n = p + 1
+    rng = np.random.default_rng(11)
+    Q = np.empty((mesh.ncells, 4, n, n))
+    Q[:, 0] = 1.0 + 0.1 * rng.random((mesh.ncells, n, n))
+    Q[:, 1] = 0.2 * rng.standard_normal((mesh.ncells, n, n))
+    Q[:, 2] = 0.2 * rng.standard_normal((mesh.ncells, n, n))
+    Q[:, 3] = 2.5 + 0.1 * rng.random((mesh.ncells, n, n))
+    h = 1.0 / 9
+    out = edg.kernels.stp_picard_batch(torch.from_numpy(Q).cuda(), pde, 0.2 * h / 7, b, (h, h))
+    tq, tf = out["trace_q"], out["trace_f"]
+    dec = decompose(mesh, R)
+    faces, keys = interior_faces(mesh)
+    axis = np.array([k[0] for k in keys])
+    plans = [exchange_plan(mesh, dec, r) for r in range(R)]
+    sent = {(r, q): pack_boundary_traces(plans[r], q, tq, tf) for r in range(R) for q in plans[r].peers}
+    outcome = {}
+    for r in range(R):
+        for q in plans[r].peers:
+            own, recv = sent[(r, q)][:, 0], sent[(q, r)][:, 0]          # trace_q rows (k, m*n)
+            lo_mine = torch.from_numpy(plans[r].local_side[q] == 0).cuda()[:, None]
+            lo, hi = torch.where(lo_mine, own, recv), torch.where(lo_mine, recv, own)
+            res = torch.empty_like(lo)
+            ax = axis[plans[r].faces[q]]
+            for a in range(2):
+                sel = torch.from_numpy(np.nonzero(ax == a)[0]).cuda()
+                res[sel] = edg.kernels.riemann_rusanov_batch(lo[sel].reshape(-1, 4, n).contiguous(),
+                                                             hi[sel].reshape(-1, 4, n).contiguous(),
+                                                             pde, a).reshape(-1, 4 * n)
+            outcome[(r, q)] = res
+            # single-domain reference for the same faces
+            f = plans[r].faces[q]
+            for a in range(2):
+                fa = f[ax == a]
+                if fa.size == 0:
+                    continue
+                lo1 = tq[torch.from_numpy(faces[fa, 0]).cuda(), 2 * a + 1].contiguous()
+                hi1 = tq[torch.from_numpy(faces[fa, 1]).cuda(), 2 * a].contiguous()
+                want = edg.kernels.riemann_rusanov_batch(lo1, hi1, pde, a).reshape(-1, 4 * n)
+                assert torch.equal(res[torch.from_numpy(np.nonzero(ax == a)[0]).cuda()], want)
+    for r in range(R):
+        for q in plans[r].peers:
+            assert torch.equal(outcome[(r, q)], outcome[(q, r)])
