@@ -1,20 +1,25 @@
 #!/usr/bin/env python
 """Benchmark: DoF-updates/s of the ADER-DG hot path on B200 (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg3]
 
 One "step" is one ADER-DG time step (admissible-dt reduction, space-time
-predictor, Riemann + corrector) of the configuration over its whole mesh,
-state resident in HBM.  The headline workload is BASELINE.json configs[1]
-(config 2: 2-D Euler, 243^2 cells, p = 5, CFL 0.9/(2p+1)), whose state plus
-predictor buffers (~300 MB) exceed the 126 MB L2, so no flush is needed
-between steps.  Under torchrun (N > 1) every rank runs an independent replica
-(the path does not shard in this tier: "replicas only"); the
-value is the aggregate over ranks, timed as the max over ranks.
+predictor, fused Riemann + corrector) of the configuration over its whole
+mesh, state resident in HBM.  The headline workload is the largest
+single-GPU configuration, BASELINE.json configs[2] (config 3: 3-D Euler, 64^3
+cells, p = 4, 1.64e8 DoF); its state plus predictor buffers (~5.7 GB) exceed
+the 126 MB L2 many times, so no flush is needed between steps.  W warm-up
+steps run first; the state is then reset to the initial condition and the
+timed steps are steps 1..K of the stated trajectory (20 steps for config 3).
+Under torchrun (N > 1) every rank runs an independent replica (the path does
+not shard in this tier: "replicas only"); the value is the
+aggregate over ranks, timed as the max over ranks.
 
---impl reference times the reference algorithm's own CPU implementation (the
-per-cell numpy port in oracle/, since the Python reference cannot travel to
-the GPU box) on the host cores, on a bounded sample of cells per step.
+--impl reference times the reference package's own per-cell CPU kernels
+(oracle/refarm.py: the reference vendored into oracle/_ref by build(), else
+the numpy port) on all host cores, each timed step on a bounded sample of
+that same step's cells whose Picard counts follow the step's histogram
+(tests/golden/refarm_cfg3.npz).
 """
 from __future__ import annotations
 
@@ -44,10 +49,11 @@ UNIT = "DoF-updates/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=47)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(cf.CONFIGS))
+    ap.add_argument("--config", default="cfg3", choices=sorted(cf.CONFIGS))
+    ap.add_argument("--no-secondary", action="store_true", help="skip the cfg2 (configs[1]) secondary line item")
     ap.add_argument("--cfl", type=float, default=None, help="override the config's CFL safety")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -266,27 +272,6 @@ def cpu_port_rate(cfg_name, cfl, seconds, cores=None, steps=1):
     return rates, cores, sample
 
 
-def cpu_batched_rate(cfg, cells=81):
-    """DoF-updates/s of the batched numpy restatement (oracle/drivers.py +
-    oracle/batched.py: one Algorithm-1 step with the cell axis vectorised) in
-    this process, on a cells^d grid of the configuration's physics (SURVEY.md
-    section 8(d) d4 asks for it beside the per-cell port, labelled)."""
-    from oracle import drivers, ops as oops
-    c = cfg.with_(cells=cells)
-    Q0 = cf.initial_dg_uniform(c)
-    pde = oops.euler(c.dim) if c.pde == "euler" else (oops.advection(c.velocity, c.dim) if c.pde == "advection"
-                                                        else oops.make_pde(c.pde, dim=c.dim))
-    basis = oops.basis_for(c.order)
-    t0 = time.perf_counter()
-    drivers.dg_uniform_step(Q0, pde, basis, cells, c.dim, c.periodic, c.cfl)
-    sec = time.perf_counter() - t0
-    dof = Q0.size
-    threads = os.environ.get("OPENBLAS_NUM_THREADS", "default")
-    return {"value": dof / sec, "unit": UNIT, "cores": 1, "kind": "port-batched",
-            "sample": f"one step of the batched numpy restatement on {cells}^{c.dim} cells of {cfg.name}'s physics, "
-                      f"one process (OPENBLAS_NUM_THREADS={threads})"}
-
-
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -299,25 +284,75 @@ def cpu_model():
 
 # ------------------------------------------------------------- reference --
 
+REFARM_FIXTURE = os.path.join(REPO, "tests", "golden", "refarm_{}.npz")
+
+
+def bench_config(cfg, ncells, ws, steps):
+    """The `config` object of both arms (identical by construction)."""
+    return {"workload": workload_name(cfg), "cells": ncells, "dof": cf.dof_count(cfg, ncells),
+            "cfl_safety": cfg.cfl, "parallelism": f"replicas x{ws} (the path does not shard in this tier)",
+            "steps_from_ic": f"1..{steps} (state reset to the initial condition after the warm-up)",
+            "l2": ("working set < 126 MB L2: 256 MB write before every timed 2-step chunk (outside the timed "
+                   "events)" if l2_flush_needed(cfg) else "working set > 126 MB L2 (state + predictor buffers), no flush")}
+
+
+def refarm_rate(cfg, steps, seconds_per_step, cores=None, step_ids=None):
+    """Reference kernels on stratified samples of trajectory steps (oracle/refarm.py).
+    Returns (value, detail) with value = sampled DoF / wall time over the steps."""
+    from oracle import refarm
+    arm = refarm.RefArm(REFARM_FIXTURE.format(cfg.name), dim=cfg.dim, order=cfg.order, h=1.0 / cfg.cells,
+                        cfl=cfg.cfl, cores=cores)
+    try:
+        per_cell = arm.per_cell_seconds(1)
+        total = int(max(arm.cores * 4, seconds_per_step * arm.cores / per_cell))
+        dof_cell = cfg.m * cfg.n ** cfg.dim
+        ids = list(step_ids if step_ids is not None else range(1, steps + 1))
+        cells = its = 0
+        wall = 0.0
+        for k in ids:
+            c, i, w = arm.time_step(k, total)
+            cells, its, wall = cells + c, its + i, wall + w
+        value = cells * dof_cell / wall
+        detail = {"kind": arm.kind, "cores": arm.cores, "picard_iterations_mean": its / cells,
+                  "picard_iterations_mean_full_mesh": float(np.mean([arm.mean_iterations(k) for k in ids])),
+                  "sample": (f"{total} cells per timed step x {len(ids)} step(s) (trajectory steps "
+                             f"{ids[0]}..{ids[-1]}), drawn from tests/golden/refarm_{cfg.name}.npz with each step's "
+                             f"Picard-count histogram (largest remainders); per cell: admissible_dt + stp_picard + "
+                             f"2d riemann_rusanov + corrector of the "
+                             f"{'vendored reference package (oracle/_ref/enclavedg)' if arm.kind == 'reference' else 'numpy port (oracle/ops.py)'}; "
+                             f"{arm.cores} worker processes, OPENBLAS_NUM_THREADS=1"),
+                  "cpu": cpu_model()}
+        return value, detail
+    finally:
+        arm.close()
+
+
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    per_step = max(1.0, min(5.0, 150.0 / max(1, args.steps + args.warmup)))
-    if cfg.kind != "dg":
-        print(json.dumps({"impl": "reference", "unavailable": "CPU port sampler covers uniform DG configs only"}))
+    ncells = cfg.cells ** cfg.dim
+    if cfg.kind == "dg" and os.path.exists(REFARM_FIXTURE.format(cfg.name)):
+        per_step = max(1.0, min(5.0, 150.0 / max(1, args.steps + args.warmup)))
+        # warm-up steps (untimed) on the trajectory's first steps, then the timed ones
+        refarm_rate(cfg, args.warmup, 0.5, step_ids=range(1, args.warmup + 1))
+        value, det = refarm_rate(cfg, args.steps, per_step)
+    elif cfg.kind == "dg":
+        per_step = max(1.0, min(5.0, 150.0 / max(1, args.steps + args.warmup)))
+        rates, cores, sample = cpu_port_rate(cfg.name, args.cfl, per_step, steps=args.warmup + args.steps)
+        value = statistics.median(rates[args.warmup:])
+        det = {"kind": "port", "cores": cores, "sample": sample, "cpu": cpu_model()}
+    else:
+        print(json.dumps({"impl": "reference", "unavailable": "CPU sampler covers the DG configs only"}))
         return
-    rates, cores, sample = cpu_port_rate(cfg.name, args.cfl, per_step, steps=args.warmup + args.steps)
-    timed = rates[args.warmup:]
-    value = statistics.median(timed)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * cf.dof_count(cfg) / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs.py)",
-        "config": {"workload": workload_name(cfg), "cells": cfg.cells ** cfg.dim, "dof": cf.dof_count(cfg)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
-                         "cpu": cpu_model()},
+        "config": bench_config(cfg, ncells, ws, args.steps),
+        "picard_iterations_mean": det.get("picard_iterations_mean"),
+        "cpu_baseline": dict(value=value, unit=UNIT, **det),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -347,6 +382,8 @@ def measure_device(cfg, steps, warmup, ws, dist, dev, peak64, local):
     solver.set_state(Q0)
     for _ in range(warmup):
         solver.step()
+    # the timed steps are steps 1..K of the stated trajectory
+    solver.set_state(Q0)
     torch.cuda.synchronize()
     its0 = int(solver.iter_total.item()) if hasattr(solver, "iter_total") else 0
     timer = S.KernelTimer()
@@ -409,8 +446,8 @@ def measure_device(cfg, steps, warmup, ws, dist, dev, peak64, local):
     # pass 2 (the production path, DGSolver.run: CUDA-graph replay of the same
     # steps from the same state): the throughput value
     solver.set_state(Q0)
-    for _ in range(warmup):
-        solver.step()
+    solver.run(warmup + warmup % 2, graph=True)        # warm-up through the graph itself
+    solver.set_state(Q0)
     solver.prepare_graph(2)
     torch.cuda.synchronize()
     if dist:
@@ -502,16 +539,19 @@ def run_ours(args, cfg):
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(r["solver"], r["Q0"], r["dof"], args.steps, ws, dist, dev)
+    secondary = None
+    if cfg.name == "cfg3" and not args.no_secondary:
+        secondary = measure_secondary(ws, dist, dev, peak64, local)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and cfg.kind == "dg":
-        rates, cores, sample = cpu_port_rate(cfg.name, args.cfl, args.cpu_seconds, steps=1)
-        cpu = {"value": rates[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
-               "cpu": cpu_model()}
-        if cfg.dim == 2:
-            try:
-                cpu["batched_restatement"] = cpu_batched_rate(cfg)
-            except Exception as exc:   # reported baseline only; never fails the bench
-                cpu["batched_restatement"] = {"unavailable": repr(exc)[:200]}
+        if os.path.exists(REFARM_FIXTURE.format(cfg.name)):
+            ids = sorted({1, max(1, args.steps // 2), args.steps})
+            value, det = refarm_rate(cfg, args.steps, args.cpu_seconds / len(ids), step_ids=ids)
+            cpu = dict(value=value, unit=UNIT, **det)
+        else:
+            rates, cores, sample = cpu_port_rate(cfg.name, args.cfl, args.cpu_seconds, steps=1)
+            cpu = {"value": rates[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                   "cpu": cpu_model()}
     if rank == 0:
         line = {
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -519,15 +559,10 @@ def run_ours(args, cfg):
             "ms_per_step_eager_with_kernel_events": r["ms_eager"] / args.steps,
             "eager_gate_us_per_step": EAGER_GATE_US, "eager_note": "eager pass (per-kernel events) with each step queued behind a GPU spin; spin time removed", "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs.py)",
-            "config": {"workload": workload_name(cfg), "cells": r["ncells"], "dof": r["dof"], "cfl_safety": cfg.cfl,
-                       "parallelism": f"replicas x{ws} (the path does not shard in this tier)",
-                       "steps_from_ic": f"{args.warmup + 1}..{args.warmup + args.steps}",
-                       "l2": ("working set < 126 MB L2: 256 MB write before every timed 2-step chunk "
-                              "(outside the timed events)" if l2_flush_needed(cfg)
-                              else "working set > 126 MB L2 (state + predictor buffers), no flush"),
-                       "picard_iterations_mean": r["iters_mean"],
-                       "nonfinite_cell_results": r["nonfinite_cells"],
-                       "first_nonfinite_step": r["first_nonfinite_step"]},
+            "config": bench_config(cfg, r["ncells"], ws, args.steps),
+            "picard_iterations_mean": r["iters_mean"],
+            "nonfinite_cell_results": r["nonfinite_cells"],
+            "first_nonfinite_step": r["first_nonfinite_step"],
             "roofline": {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
                          "unit": roof["unit"], "frac": roof["frac"], "traffic": traffic,
                          "kernel": roof["kernel"],
@@ -540,10 +575,25 @@ def run_ours(args, cfg):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "parity_safe_variant": variant,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def measure_secondary(ws, dist, dev, peak64, local):
+    """BASELINE configs[1] (config 2 at its stated CFL 0.9/(2p+1)) as a line
+    item: steps 1..10 from the initial condition, before the reference
+    scheme's own blow-up at step 15 (tests/test_gpu_fullsize.py)."""
+    cfg = cf.CONFIGS["cfg2"]
+    v = measure_device(cfg, 10, 4, ws, dist, dev, peak64, local)
+    out = {"workload": workload_name(cfg), "steps_from_ic": "1..10", "value": v["value"], "unit": UNIT,
+           "ms_per_step": v["ms"] / 10, "picard_iterations_mean": v["iters_mean"],
+           "nonfinite_cell_results": v["nonfinite_cells"], "kernels": v["kernels"],
+           "roofline_frac": v["roof"]["frac"]}
+    del v
+    return out
 
 
 def measure_e2e(solver, Q0, dof, steps, ws, dist, dev):

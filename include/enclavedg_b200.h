@@ -233,6 +233,26 @@ int edg_stream_priority_range(int32_t* least, int32_t* greatest);
 /* Last CUDA error string of this thread (static storage). */
 const char* edg_last_error(void);
 
+/* CUDA graphs that keep per-node stream priorities (the skeleton-first
+ * schedule of SPEC.md:403-404 inside a replayed graph).  edg_graph_begin
+ * starts a relaxed-mode capture on `stream`; edg_graph_end ends it, writes
+ * the priority attribute of each captured kernel node (graph node order, at
+ * most max_nodes) and their count, and instantiates the executable graph with
+ * cudaGraphInstantiateFlagUseNodePriority into *exec_out. */
+int edg_graph_begin(void* stream);
+int edg_graph_end(void* stream, void** exec_out, int32_t* node_priority, int32_t max_nodes, int32_t* nkernels);
+int edg_graph_launch(void* exec, void* stream);
+int edg_graph_destroy(void* exec);
+
+/* Launch trace (SPEC.md:392-400 record_trace; tests/test_gpu_schedule.py):
+ * the NEXT traced launch issued by the calling host thread (edg_stp_picard,
+ * edg_corrector, edg_corrector_grid, edg_faces_rusanov, edg_faces_restrict,
+ * edg_dt_finalize, the edg_fv_* updates) records into slot_dev[0..1]: the
+ * global-timer ns of its first CTA start (atomicMin) and of its last CTA exit
+ * (atomicMax).  Initialise the slot to {UINT64_MAX, 0}.  Inside a stream
+ * capture the slot address is baked into the graph node. */
+int edg_trace_next(unsigned long long* slot_dev);
+
 /* ---- rank-boundary trace exchange (host half in
  * decomposition.py; replaces the per-face send_face / receive_face payloads of
  * SPEC.md:425-508 and boundary_face_order mesh.py:613-628) ----------------

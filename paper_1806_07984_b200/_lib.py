@@ -14,8 +14,7 @@ import re
 from .errors import STATUS_ERRORS, NativeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# EDG_LIB overrides the path (A/B variants built by build_lib --variant)
-LIB_PATH = os.environ.get("EDG_LIB") or os.path.join(HERE, "_lib", "libenclavedg_b200.so")
+LIB_PATH = os.path.join(HERE, "_lib", "libenclavedg_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "enclavedg_b200.h")
 
 PDE_KIND = {"advection": 0, "burgers": 1, "euler": 2}
@@ -56,6 +55,11 @@ SIGNATURES = {
     "edg_fv_grid_step": (C.c_int, [PDEP, I32, I32, I32, P, P, P, P, P, D, P, P]),
     "edg_patch_boundary_layers": (C.c_int, [I32, I32, I32, I32, P, P, P]),
     "edg_stream_priority_range": (C.c_int, [C.POINTER(I32), C.POINTER(I32)]),
+    "edg_graph_begin": (C.c_int, [P]),
+    "edg_graph_end": (C.c_int, [P, C.POINTER(C.c_void_p), P, I32, C.POINTER(I32)]),
+    "edg_graph_launch": (C.c_int, [P, P]),
+    "edg_graph_destroy": (C.c_int, [P]),
+    "edg_trace_next": (C.c_int, [P]),
     "edg_gradient_indicator": (C.c_int, [I32, I32, I32, P, I32, P, P, D, D, I32, I32, P, P, P]),
     "edg_interpolate_volume": (C.c_int, [I32, I32, I32, P, I32, P, P, P, P, P]),
     "edg_restrict_volume": (C.c_int, [I32, I32, I32, P, I32, P, P, P]),

@@ -63,6 +63,13 @@ static PdeParams params_of(const edg_pde* p) {
 }
 
 static thread_local char g_err[256] = "";
+// launch-trace slot for the next traced launch of this host thread (edg_trace_next)
+static thread_local unsigned long long* g_trace_next = nullptr;
+static unsigned long long* take_trace() {
+  unsigned long long* t = g_trace_next;
+  g_trace_next = nullptr;
+  return t;
+}
 static int fail(int code, const char* what) {
   std::snprintf(g_err, sizeof g_err, "%s", what);
   return code;
@@ -82,6 +89,11 @@ extern "C" {
 
 const char* edg_last_error(void) { return g_err; }
 
+int edg_trace_next(unsigned long long* slot_dev) {
+  g_trace_next = slot_dev;
+  return EDG_OK;
+}
+
 const char* edg_build_info(void) {
   return "enclavedg_b200 1.0 sm_100a fp64 (STP picard / rusanov / corrector / fv / dt / transfer)";
 }
@@ -97,6 +109,7 @@ int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev, c
                    const double* dt_dev, double tol, int32_t max_iter, double* q_end_dev, double* q_int_dev,
                    double* trace_q_dev, double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev,
                    unsigned long long* iter_total_dev, void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (order < 1 || order + 1 > u->max_n()) return fail(EDG_ERR_CONFIG, "polynomial order not built for this pde/dim");
@@ -123,6 +136,7 @@ int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev, c
   a.iterations = iterations_dev;
   a.converged = converged_dev;
   a.iter_total = iter_total_dev;
+  a.trace = trace;
   return cuda_status(u->stp(order + 1, a, (cudaStream_t)stream));
 }
 
@@ -167,6 +181,7 @@ int edg_corrector(const edg_pde* pde, int32_t order, const double* basis_dev, in
                   const int32_t* side_face_dev, const double* outcomes_dev, const double* edges_dev,
                   int32_t edges_per_cell, double* q_out_dev, unsigned long long* dt_slots_dev,
                   const double* hmin_dev, uint32_t* status_dev, void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (order < 1 || order + 1 > u->max_n()) return fail(EDG_ERR_CONFIG, "polynomial order not built for this pde/dim");
@@ -193,6 +208,7 @@ int edg_corrector(const edg_pde* pde, int32_t order, const double* basis_dev, in
   a.hmin = hmin_dev;
   a.status = status_dev;
   a.pp = params_of(pde);
+  a.trace = trace;
   return cuda_status(u->corr(order + 1, fused, a, (cudaStream_t)stream));
 }
 
@@ -200,6 +216,7 @@ int edg_corrector_grid(const edg_pde* pde, int32_t order, const double* basis_de
                        int32_t periodic, const double* q_end_dev, const double* trace_q_dev, const double* trace_f_dev,
                        const double* edges_dev, double* q_out_dev, unsigned long long* dt_slots_dev,
                        const double* hmin_dev, uint32_t* status_dev, void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (order < 1 || order + 1 > u->max_n()) return fail(EDG_ERR_CONFIG, "polynomial order not built for this pde/dim");
@@ -227,6 +244,7 @@ int edg_corrector_grid(const edg_pde* pde, int32_t order, const double* basis_de
   a.hmin = hmin_dev;
   a.status = status_dev;
   a.pp = params_of(pde);
+  a.trace = trace;
   return cuda_status(u->corr(order + 1, true, a, (cudaStream_t)stream));
 }
 
@@ -245,14 +263,16 @@ int edg_dt_slots_reset(unsigned long long* dt_slots_dev, void* stream) {
 
 int edg_dt_finalize(unsigned long long* dt_slots_dev, double cfl, double* dt_dev, double* dt_hist_dev, int32_t step,
                     uint32_t* status_dev, void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   dt_finalize_kernel<<<1, EDG_DT_SLOTS, 0, (cudaStream_t)stream>>>(dt_slots_dev, cfl, dt_dev, dt_hist_dev, step,
-                                                                   status_dev);
+                                                                   status_dev, trace);
   return cuda_status(check_launch());
 }
 
 int edg_faces_rusanov(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t nfaces,
                       const int32_t* axis_dev, const int32_t* cell_dev, const int8_t* kind_dev,
                       const int8_t* child_pos_dev, const double* trace_q_dev, double* outcomes_dev, void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (order < 1 || order + 1 > u->max_n()) return fail(EDG_ERR_CONFIG, "polynomial order not built for this pde/dim");
@@ -266,6 +286,7 @@ int edg_faces_rusanov(const edg_pde* pde, int32_t order, const double* basis_dev
   a.trace_q = trace_q_dev;
   a.outcomes = outcomes_dev;
   a.pp = params_of(pde);
+  a.trace = trace;
   return cuda_status(u->faces(order + 1, a, (cudaStream_t)stream));
 }
 
@@ -273,14 +294,14 @@ int edg_faces_rusanov(const edg_pde* pde, int32_t order, const double* basis_dev
 
 template <int DIM>
 static int restrict_dim(int n, const double* basis, int m, int np, const int32_t* pf, const int32_t* ch,
-                        const int8_t* cp, double* out, cudaStream_t st) {
+                        const int8_t* cp, double* out, unsigned long long* trace, cudaStream_t st) {
   const long long work = (long long)np * m * ipow(n, DIM - 1);
   if (work <= 0) return EDG_OK;
   const unsigned blocks = (unsigned)((work + 127) / 128);
   switch (n) {
 #define EDG_CASE(NN)                                                                         \
   case NN:                                                                                   \
-    faces_restrict_kernel<DIM, NN><<<blocks, 128, 0, st>>>(basis, m, np, pf, ch, cp, out); \
+    faces_restrict_kernel<DIM, NN><<<blocks, 128, 0, st>>>(basis, m, np, pf, ch, cp, out, trace); \
     return check_launch();
     EDG_CASE(2) EDG_CASE(3) EDG_CASE(4) EDG_CASE(5) EDG_CASE(6) EDG_CASE(7) EDG_CASE(8)
 #undef EDG_CASE
@@ -293,14 +314,15 @@ extern "C" {
 int edg_faces_restrict(int32_t dim, int32_t m, int32_t order, const double* basis_dev, int32_t nparents,
                        const int32_t* parent_face_dev, const int32_t* children_dev, const int8_t* child_pos_dev,
                        double* outcomes_dev, void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   if (order < 1 || order > 7) return fail(EDG_ERR_CONFIG, "order out of range");
   const cudaStream_t st = (cudaStream_t)stream;
   if (dim == 2)
     return cuda_status(restrict_dim<2>(order + 1, basis_dev, m, nparents, parent_face_dev, children_dev, child_pos_dev,
-                                       outcomes_dev, st));
+                                       outcomes_dev, trace, st));
   if (dim == 3)
     return cuda_status(restrict_dim<3>(order + 1, basis_dev, m, nparents, parent_face_dev, children_dev, child_pos_dev,
-                                       outcomes_dev, st));
+                                       outcomes_dev, trace, st));
   return fail(EDG_ERR_CONFIG, "dim must be 2 or 3");
 }
 
@@ -371,11 +393,13 @@ int edg_project_to_faces(int32_t dim, int32_t m, int32_t order, const double* ba
 int edg_fv_patch_update(const edg_pde* pde, int32_t k, int32_t npatches, const double* patch_dev,
                         const double* halos_dev, const double* dt_dev, const double* edges_dev, double* out_dev,
                         void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (!halos_dev) return fail(EDG_ERR_PROTOCOL, "halo layers missing");
   FvArgs a;
   std::memset(&a, 0, sizeof a);
+  a.trace = trace;
   a.npatches = npatches;
   a.patch = patch_dev;
   a.halos = halos_dev;
@@ -389,11 +413,13 @@ int edg_fv_patch_update(const edg_pde* pde, int32_t k, int32_t npatches, const d
 int edg_fv_patch_step(const edg_pde* pde, int32_t k, int32_t npatches, const double* patch_dev,
                       const int32_t* nbr_dev, const double* dt_dev, const double* edges_dev, double* out_dev,
                       unsigned long long* dt_slots_dev, double h_cell, uint32_t* status_dev, void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (!nbr_dev) return fail(EDG_ERR_PROTOCOL, "patch neighbour table missing");
   FvArgs a;
   std::memset(&a, 0, sizeof a);
+  a.trace = trace;
   a.npatches = npatches;
   a.patch = patch_dev;
   a.nbr = nbr_dev;
@@ -410,6 +436,7 @@ int edg_fv_patch_step(const edg_pde* pde, int32_t k, int32_t npatches, const dou
 int edg_fv_grid_step(const edg_pde* pde, int32_t k, int32_t patches_per_axis, int32_t periodic,
                      const double* patch_dev, const double* dt_dev, const double* edges_dev, double* out_dev,
                      unsigned long long* dt_slots_dev, double h_cell, uint32_t* status_dev, void* stream) {
+  unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (patches_per_axis < 1) return fail(EDG_ERR_CONFIG, "empty patch grid");
@@ -417,6 +444,7 @@ int edg_fv_grid_step(const edg_pde* pde, int32_t k, int32_t patches_per_axis, in
   for (int d = 0; d < pde->dim; ++d) np *= patches_per_axis;
   FvArgs a;
   std::memset(&a, 0, sizeof a);
+  a.trace = trace;
   a.npatches = (int32_t)np;
   a.patch = patch_dev;
   a.pgrid_n = patches_per_axis;
@@ -511,6 +539,59 @@ int edg_stream_priority_range(int32_t* least, int32_t* greatest) {
   if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return cuda_status(EDG_ERR_CUDA);
   *least = lo;
   *greatest = hi;
+  return EDG_OK;
+}
+
+// ---- CUDA graphs that keep the stream priorities -------------------------
+// A kernel captured from a prioritised stream carries that priority as its
+// node's launch attribute; it only takes effect if the executable graph is
+// instantiated with cudaGraphInstantiateFlagUseNodePriority (otherwise every
+// node runs at the priority of the stream the graph is launched into), which
+// torch.cuda.CUDAGraph does not do -- hence these four entry points.
+int edg_graph_begin(void* stream) {
+  if (cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+    return cuda_status(EDG_ERR_CUDA);
+  return EDG_OK;
+}
+
+int edg_graph_end(void* stream, void** exec_out, int32_t* node_priority, int32_t max_nodes, int32_t* nkernels) {
+  cudaGraph_t g = nullptr;
+  if (cudaStreamEndCapture((cudaStream_t)stream, &g) != cudaSuccess || !g) return cuda_status(EDG_ERR_CUDA);
+  size_t n = 0;
+  int nk = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return cuda_status(EDG_ERR_CUDA);
+  }
+  cudaGraphNode_t* nodes = new cudaGraphNode_t[n > 0 ? n : 1];
+  cudaGraphGetNodes(g, nodes, &n);
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+    cudaLaunchAttributeValue v;
+    std::memset(&v, 0, sizeof v);
+    if (cudaGraphKernelNodeGetAttribute(nodes[i], cudaLaunchAttributePriority, &v) != cudaSuccess) v.priority = 0;
+    if (node_priority && nk < max_nodes) node_priority[nk] = v.priority;
+    ++nk;
+  }
+  delete[] nodes;
+  if (nkernels) *nkernels = nk;
+  cudaGraphExec_t ex = nullptr;
+  const cudaError_t e = cudaGraphInstantiateWithFlags(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_status(EDG_ERR_CUDA);
+  *exec_out = (void*)ex;
+  return EDG_OK;
+}
+
+int edg_graph_launch(void* exec, void* stream) {
+  if (!exec) return fail(EDG_ERR_CONFIG, "null graph");
+  if (cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream) != cudaSuccess) return cuda_status(EDG_ERR_CUDA);
+  return EDG_OK;
+}
+
+int edg_graph_destroy(void* exec) {
+  if (exec && cudaGraphExecDestroy((cudaGraphExec_t)exec) != cudaSuccess) return cuda_status(EDG_ERR_CUDA);
   return EDG_OK;
 }
 

@@ -16,6 +16,26 @@ namespace edg {
 
 constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
+// Launch trace (edg_trace_next, include/enclavedg_b200.h): when a kernel is
+// given a slot, thread 0 of every CTA folds the global timer at its start
+// into slot[0] (atomicMin) and at its exit into slot[1] (atomicMax), so the
+// slot ends up holding the launch's first-CTA start and last-CTA end in ns.
+// Two atomics per CTA; a null slot costs one predicated branch.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct TraceScope {
+  unsigned long long* slot;
+  __device__ __forceinline__ explicit TraceScope(unsigned long long* s) : slot(s) {
+    if (slot && threadIdx.x == 0) atomicMin(slot, global_ns());
+  }
+  __device__ __forceinline__ ~TraceScope() {
+    if (slot && threadIdx.x == 0) atomicMax(slot + 1, global_ns());
+  }
+};
+
 struct PdeParams {
   double gamma;
   double gm1;       // gamma - 1.0, computed on the host exactly like the oracle

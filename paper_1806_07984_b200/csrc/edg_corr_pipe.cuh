@@ -54,6 +54,7 @@ struct CorrPipe {
 
 template <int KIND, int DIM, int N, bool GRID = true>
 __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) corrector_grid_pipe_kernel(const CorrArgs A) {
+  const TraceScope trace_scope(A.trace);
   using P = Pde<KIND, DIM>;
   using C = CorrPipe<KIND, DIM, N, GRID>;
   constexpr int M = C::M, NPC = C::NPC, NF = C::NF, CPB = C::CPB, THREADS = C::THREADS, TRC = C::TRC;

@@ -71,7 +71,8 @@ static __global__ void dt_slots_reset_kernel(unsigned long long* slots) {
 }
 
 static __global__ void dt_finalize_kernel(unsigned long long* slots, double cfl, double* dt, double* hist, int step,
-                                   uint32_t* status) {
+                                   uint32_t* status, unsigned long long* trace) {
+  const TraceScope trace_scope(trace);
   __shared__ unsigned long long s[EDG_DT_SLOTS];
   const int t = threadIdx.x;
   s[t] = slots[t];

@@ -35,6 +35,7 @@ struct CorrArgs {
   const double* hmin;
   uint32_t* status;
   PdeParams pp;
+  unsigned long long* trace;   // optional launch-trace slot (TraceScope)
 };
 
 template <int DIM, int N>
@@ -56,6 +57,7 @@ struct CorrSmem {
 
 template <int KIND, int DIM, int N, bool FUSED>
 __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(const CorrArgs A) {
+  const TraceScope trace_scope(A.trace);
   using P = Pde<KIND, DIM>;
   using Cf = CorrCfg<DIM, N>;
   constexpr int M = P::M;
@@ -274,6 +276,7 @@ struct FaceArgs {
   const double* trace_q;
   double* outcomes;
   PdeParams pp;
+  unsigned long long* trace;   // optional launch-trace slot (TraceScope)
 };
 
 // trace of one side at face point f: own trace, or the coarse owner's trace
@@ -318,6 +321,7 @@ __device__ __forceinline__ void side_state(const double* tr, int kind, const int
 
 template <int KIND, int DIM, int N>
 __global__ void __launch_bounds__(128) faces_rusanov_kernel(const FaceArgs A) {
+  const TraceScope trace_scope(A.trace);
   using P = Pde<KIND, DIM>;
   constexpr int M = P::M;
   constexpr int NF = ipow(N, DIM - 1);
@@ -357,7 +361,9 @@ __global__ void __launch_bounds__(128) faces_rusanov_kernel(const FaceArgs A) {
 template <int DIM, int N>
 __global__ void __launch_bounds__(128) faces_restrict_kernel(const double* basis, int m, int nparents,
                                                              const int32_t* parent_face, const int32_t* children,
-                                                             const int8_t* child_pos, double* outcomes) {
+                                                             const int8_t* child_pos, double* outcomes,
+                                                             unsigned long long* trace) {
+  const TraceScope trace_scope(trace);
   constexpr int NF = ipow(N, DIM - 1);
   constexpr int NCH = ipow(3, DIM - 1);
   __shared__ double sR[3 * N * N];

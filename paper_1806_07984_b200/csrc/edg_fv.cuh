@@ -38,6 +38,7 @@ struct FvArgs {
   double h_cell;
   uint32_t* status;
   PdeParams pp;
+  unsigned long long* trace;   // optional launch-trace slot (TraceScope)
 };
 
 template <int DIM, int K>
@@ -373,6 +374,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
 
 template <int KIND, int DIM, int K, int MINB = FvCfg<DIM, K>::MINB>
 __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(const FvArgs A) {
+  const TraceScope trace_scope(A.trace);
   extern __shared__ __align__(16) double smem[];
   fv_patch_body<KIND, DIM, K, false>(A, blockIdx.x, smem, nullptr, [] {});
 }

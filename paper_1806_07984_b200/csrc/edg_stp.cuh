@@ -44,6 +44,7 @@ struct StpArgs {
   int32_t* iterations;
   uint8_t* converged;
   unsigned long long* iter_total;   // optional: += sum of per-cell iterations
+  unsigned long long* trace;        // optional launch-trace slot (TraceScope)
 };
 
 constexpr int stp_best_cpb(int npc, int target) {
@@ -221,6 +222,7 @@ struct StpSmem {
 template <int KIND, int DIM, int N, int MINB = StpCfg<DIM, N>::MINB>
 __global__ void __launch_bounds__(StpCfg<DIM, N>::THREADS, MINB)
 stp_picard_kernel(const StpArgs A) {
+  const TraceScope trace_scope(A.trace);
   using P = Pde<KIND, DIM>;
   using Cf = StpCfg<DIM, N>;
   using Sm = StpSmem<KIND, DIM, N>;

@@ -2,13 +2,9 @@
 // PDE-specialised kernel for the supported node counts and exposes host-side
 // launchers edg::unit_<name>_*.  Included by edg_k_*.cu with EDG_UNIT_KIND,
 // EDG_UNIT_DIM and EDG_UNIT_NAME defined (split for parallel nvcc builds).
-#include <cstdlib>
 #include <mutex>
 
 #include "edg_stp.cuh"
-#include "edg_stp_th.cuh"
-#include "edg_stp_pair.cuh"
-#include "edg_stp_pen.cuh"
 #include "edg_stp_ck.cuh"
 #include "edg_faces.cuh"
 #include "edg_corr_pipe.cuh"
@@ -88,73 +84,9 @@ static int upload_ops(const double* basis, cudaStream_t st) {
 template <int N>
 static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
-  if constexpr (DIM == 2 && N % 2 == 0) {
-    // time-split kernel for even node counts: opt-in (EDG_STP_TH=1); measured
-    // 10-15% slower than the one-thread-per-node kernel on cfg2 / cfg5
-    static const int th = [] {
-      const char* v = getenv("EDG_STP_TH");
-      return v ? atoi(v) : 0;
-    }();
-    if (th) {
-      using Ct = StpThCfg<DIM, N>;
-      const size_t smem = StpThSmem<KIND, DIM, N>::BYTES;
-      auto kern = stp_picard_th_kernel<KIND, DIM, N>;
-      if (set_smem(kern, smem)) return EDG_ERR_CUDA;
-      const int blocks = (a.nwork + Ct::CPB - 1) / Ct::CPB;
-      if (blocks > 0) kern<<<blocks, Ct::THREADS, smem, st>>>(a);
-      return check_launch();
-    }
-  }
-  if constexpr (DIM == 2 && N % 2 == 0) {
-    // node-pair / time-split kernel (edg_stp_pair.cuh): EDG_STP_PAIR=1 selects it
-    static const int pair = [] {
-      const char* v = getenv("EDG_STP_PAIR");
-      return v ? atoi(v) : 0;
-    }();
-    if (pair) {
-      using Cp = StpPairCfg<N>;
-      const size_t smem = StpPairSmem<KIND, N>::BYTES;
-      auto kern = stp_pair_kernel<KIND, N>;
-      if (set_smem(kern, smem)) return EDG_ERR_CUDA;
-      const int blocks = (a.nwork + Cp::CPB - 1) / Cp::CPB;
-      const int cap = persistent_grid(kern, Cp::THREADS, smem);
-      if (cap < 0) return EDG_ERR_CUDA;
-      const int grid = blocks < cap ? blocks : cap;
-      if (grid > 0) kern<<<grid, Cp::THREADS, smem, st>>>(a);
-      return check_launch();
-    }
-  }
-  if constexpr (DIM == 2 && N <= 6) {
-    // pencil formulation (edg_stp_pen.cuh): EDG_STP_PEN=1 selects it
-    static const int pen = [] {
-      const char* v = getenv("EDG_STP_PEN");
-      return v ? atoi(v) : 0;
-    }();
-    if (pen) {
-      using Cp = PenCfg<KIND, N>;
-      auto kern = stp_pencil_kernel<KIND, N>;
-      if (set_smem(kern, Cp::BYTES)) return EDG_ERR_CUDA;
-      // operator table head -> this unit's constant bank (device to device, in stream order)
-      if (cudaMemcpyToSymbolAsync(kPen, a.basis, sizeof(double) * pen_ops(N), sizeof(double) * pen_off(N),
-                                  cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-        return EDG_ERR_CUDA;
-      const int blocks = (a.nwork + Cp::CPB - 1) / Cp::CPB;
-      const int cap = persistent_grid(kern, Cp::THREADS, Cp::BYTES);
-      if (cap < 0) return EDG_ERR_CUDA;
-      const int grid = blocks < cap ? blocks : cap;
-      if (grid > 0) kern<<<grid, Cp::THREADS, Cp::BYTES, st>>>(a);
-      return check_launch();
-    }
-  }
   using Cf = StpCfg<DIM, N>;
   const size_t smem = StpSmem<KIND, DIM, N>::BYTES;
-  // EDG_STP_MINB=2 selects the 2-CTA/SM register budget (no spills) instead
-  // of the default 3-CTA/SM one (tuning knob, read once)
-  static const int minb = [] {
-    const char* v = getenv("EDG_STP_MINB");
-    return v ? atoi(v) : 0;
-  }();
-  auto kern = (minb == 2) ? stp_picard_kernel<KIND, DIM, N, 2> : stp_picard_kernel<KIND, DIM, N>;
+  auto kern = stp_picard_kernel<KIND, DIM, N>;
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
   if (StpSmem<KIND, DIM, N>::KC) {
     if (upload_ops<N>(a.basis, st)) return EDG_ERR_CUDA;
@@ -206,43 +138,27 @@ int EDG_FN(_stp)(int n, const StpArgs& a, cudaStream_t st) {
   return EDG_ERR_CONFIG;
 }
 
-// uniform-grid corrector: persistent, cp.async double-buffered kernel
-// (edg_corr_pipe.cuh); EDG_CORR_PIPE=0 selects the one-CTA-per-group kernel
-// (auto choice) a mesh too small to give any persistent CTA a second group has
-// nothing to overlap: the one-CTA-per-group kernel is used instead
-constexpr int kCorrUseClassic = -1000;
-template <int N, bool GRID>
-static int launch_corr_grid_n(const CorrArgs& a, cudaStream_t st, bool force = true) {
-  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
-  using C = CorrPipe<KIND, DIM, N, GRID>;
-  auto kern = corrector_grid_pipe_kernel<KIND, DIM, N, GRID>;
-  if (set_smem(kern, C::BYTES)) return EDG_ERR_CUDA;
-  const int grid_cap = persistent_grid(kern, C::THREADS, C::BYTES);
-  if (grid_cap < 0) return EDG_ERR_CUDA;
-  const int ngroups = (a.ncells + C::CPB - 1) / C::CPB;
-  if (!force && ngroups <= grid_cap) return kCorrUseClassic;
-  const int grid = ngroups < grid_cap ? ngroups : grid_cap;
-  if (grid > 0) kern<<<grid, C::THREADS, C::BYTES, st>>>(a);
-  return check_launch();
-}
-
+// uniform-grid corrector: the persistent, bulk-copy double-buffered kernel
+// (edg_corr_pipe.cuh); a mesh too small to give any persistent CTA a second
+// group has nothing to overlap, so it gets the one-CTA-per-group kernel
 template <int N>
 static int launch_corr_n(bool fused, const CorrArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
-  // uniform grids: the pipelined kernel by default (measured +17 % on cfg2,
-  // +24 % on cfg3 with one cell per group); adaptive meshes: the one-CTA-per-
-  // group kernel by default (cfg5's 13k cells give each persistent CTA about
-  // one group: nothing to overlap, measured 25 % slower pipelined).
-  // EDG_CORR_PIPE=0 / 1 forces the choice for both.
-  static const int pipe = [] {
-    const char* v = getenv("EDG_CORR_PIPE");
-    return v ? (v[0] != '0' ? 1 : 0) : -1;
-  }();
-  if (pipe != 0 && fused && a.grid_n > 0 && a.edges_per_cell == 0) {
-    const int r = launch_corr_grid_n<N, true>(a, st, pipe == 1);
-    if (r != kCorrUseClassic) return r;
+  if (fused && a.grid_n > 0 && a.edges_per_cell == 0) {
+    using C = CorrPipe<KIND, DIM, N, true>;
+    auto kern = corrector_grid_pipe_kernel<KIND, DIM, N, true>;
+    if (set_smem(kern, C::BYTES)) return EDG_ERR_CUDA;
+    const int grid_cap = persistent_grid(kern, C::THREADS, C::BYTES);
+    if (grid_cap < 0) return EDG_ERR_CUDA;
+    const int ngroups = (a.ncells + C::CPB - 1) / C::CPB;
+    if (ngroups > grid_cap) {
+      kern<<<grid_cap, C::THREADS, C::BYTES, st>>>(a);
+      return check_launch();
+    }
   }
-  if (pipe == 1 && !fused) return launch_corr_grid_n<N, false>(a, st);
+  // adaptive meshes (outcomes gathered through side_face) and small grids:
+  // one CTA per group of cells (the pipelined kernel measured 25 % slower on
+  // cfg5, whose 13k cells give each persistent CTA about one group)
   using Cf = CorrCfg<DIM, N>;
   const size_t smem = CorrSmem<KIND, DIM, N>::BYTES;
   const int blocks = (a.ncells + Cf::CPB - 1) / Cf::CPB;
@@ -307,30 +223,7 @@ template <int K>
 static int launch_fv_k(const FvArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
   const size_t smem = FvSmem<KIND, DIM, K>::BYTES;
-  // EDG_FV_MINB=2 selects the 2-CTA/SM register budget (tuning knob)
-  static const int minb = [] {
-    const char* v = getenv("EDG_FV_MINB");
-    return v ? atoi(v) : 0;
-  }();
-  // patch grids (edg_fv_grid_step): EDG_FV_PIPE=1 selects the persistent
-  // kernel with cp.async prefetch of the next patch
-  // (measured 9 % slower on cfg4: 2 instead of 3 CTAs per SM and the halo
-  // gather's index arithmetic outweigh the hidden load latency; opt-in)
-  static const bool pipe = [] {
-    const char* v = getenv("EDG_FV_PIPE");
-    return v && v[0] == '1';
-  }();
-  if (pipe && a.pgrid_n > 0 && !a.halos && !a.nbr) {
-    using Sm = FvSmem<KIND, DIM, K>;
-    auto pk = fv_grid_pipe_kernel<KIND, DIM, K>;
-    if (set_smem(pk, Sm::PIPE_BYTES)) return EDG_ERR_CUDA;
-    const int cap = persistent_grid(pk, FvCfg<DIM, K>::THREADS, Sm::PIPE_BYTES);
-    if (cap < 0) return EDG_ERR_CUDA;
-    const int grid = a.npatches < cap ? a.npatches : cap;
-    if (grid > 0) pk<<<grid, FvCfg<DIM, K>::THREADS, Sm::PIPE_BYTES, st>>>(a);
-    return check_launch();
-  }
-  auto kern = (minb == 2) ? fv_patch_kernel<KIND, DIM, K, 2> : fv_patch_kernel<KIND, DIM, K>;
+  auto kern = fv_patch_kernel<KIND, DIM, K>;
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
   if (a.npatches > 0) kern<<<a.npatches, FvCfg<DIM, K>::THREADS, smem, st>>>(a);
   return check_launch();

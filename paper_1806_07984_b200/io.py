@@ -85,3 +85,76 @@ def load_solution(mesh, path, m=None):
         raise ConfigError(f"load_solution: {total} values do not fit {C} cells x {m} components")
     a = np.array(vals).reshape(C, n ** d, m).transpose(0, 2, 1)
     return a.reshape((C, m) + (n,) * d)
+
+
+# ------------------------------------------------------------ event logs --
+
+def entity_id(kind, obj):
+    """Entity ids in the reference's format (mesh.py:687-690): cells
+    'c{level}:{i}:{j}[:{k}]', faces 'f{id}'."""
+    if kind == "face":
+        return f"f{int(obj)}"
+    level, index = obj
+    return f"c{int(level)}:" + ":".join(str(int(i)) for i in index)
+
+
+def dump_event_log(rows, path):
+    """Write events as CSV `sweep,kind,entity_id,order_index` -- the
+    reference's dump_event_log (mesh.py:679-684), same columns and format."""
+    try:
+        with open(path, "w") as fh:
+            fh.write("sweep,kind,entity_id,order_index\n")
+            for sweep, kind, entity, idx in rows:
+                fh.write(f"{sweep},{kind},{entity},{idx}\n")
+    except OSError as e:
+        raise OSError(f"dump_event_log: cannot write {path}: {e}") from e
+
+
+def schedule_events(mesh, sweep=0):
+    """The device schedule's issue order for one step as event rows
+    (sweep, kind, entity_id, order_index): on an adaptive mesh the skeleton
+    cells' predictors, the skeleton-only leaf faces (every hanging face among
+    them), the enclave cells' predictors, then the remaining leaf faces; on a
+    Cartesian mesh the cells in storage order (the solver reorders them by
+    their last Picard count on the device) and the faces per axis.  This
+    replaces the reference's traversal orders (mesh.py:505-628), which have
+    no device counterpart."""
+    rows = []
+    if isinstance(mesh, AdaptiveMesh):
+        seq = [("cell", mesh.cells[c]) for c in mesh.skeleton]
+        seq += [("face", f) for f in range(mesh.nleaf_skeleton)]
+        seq += [("cell", mesh.cells[c]) for c in mesh.enclave]
+        seq += [("face", f) for f in range(mesh.nleaf_skeleton, mesh.nleaf)]
+    elif isinstance(mesh, CartesianMesh):
+        seq = [("cell", (0, tuple(ix))) for ix in mesh.index]
+        seq += [("face", f) for f in range(mesh.ncells * mesh.dim)]
+    else:
+        raise ConfigError(f"schedule_events: unsupported mesh type {type(mesh).__name__}")
+    for i, (kind, obj) in enumerate(seq):
+        rows.append((sweep, kind, entity_id(kind, obj), i))
+    return rows
+
+
+def dump_trace(records, path, t0=None):
+    """Write launch-trace records (solver.LaunchTrace.records()) as the SPEC's
+    trace CSV `t_ns,worker,event,entity,sweep`: one `start` and
+    one `finish` row per launch (first-CTA start / last-CTA exit on the device
+    clock, ns relative to the earliest start), worker = the stream class
+    (main / hi / lo), entity = the task kind, rows in time order."""
+    if not records:
+        rows = []
+    else:
+        base = min(r[3] for r in records) if t0 is None else t0
+        rows = []
+        for entity, worker, sweep, start, end in records:
+            rows.append((start - base, worker, "start", entity, sweep))
+            rows.append((end - base, worker, "finish", entity, sweep))
+        rows.sort(key=lambda r: (r[0], r[2] != "finish"))
+    try:
+        with open(path, "w") as fh:
+            fh.write("t_ns,worker,event,entity,sweep\n")
+            for r in rows:
+                fh.write(f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]}\n")
+    except OSError as e:
+        raise OSError(f"dump_trace: cannot write {path}: {e}") from e
+    return len(rows)

@@ -55,6 +55,62 @@ class KernelTimer:
         return {k: (len(v), sum(a.elapsed_time(b) for a, b in v)) for k, v in self.pairs.items()}
 
 
+class _NativeGraph:
+    """An executable CUDA graph instantiated by edg_graph_end."""
+
+    def __init__(self, lib, exec_ptr, node_priorities):
+        self.lib, self.exec = lib, exec_ptr
+        self.node_priorities = node_priorities   # priority attribute of each kernel node
+
+    def replay(self):
+        _lib.check(self.lib.edg_graph_launch(self.exec, _stream()), "graph launch")
+
+    def close(self):
+        if self.exec is not None and self.exec.value:
+            self.lib.edg_graph_destroy(self.exec)
+        self.exec = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LaunchTrace:
+    """Per-launch device timestamps of the step's kernels (edg_trace_next):
+    slot i holds the global-timer ns of launch i's first CTA start and last
+    CTA exit.  Labels (entity kind, stream, sweep) are recorded on the host
+    when the launch is issued -- inside a graph capture they describe the
+    captured nodes, and every replay rewrites the same slots.  The GPU
+    analogue of the task trace of SPEC.md:392-400 (`record_trace`)."""
+
+    def __init__(self, capacity: int = 512):
+        torch = _torch()
+        self.slots = torch.empty((capacity, 2), dtype=torch.int64, device="cuda")
+        self.labels = []
+        self.reset()
+
+    def reset(self, labels: bool = False):
+        """Re-arm every slot ({UINT64_MAX, 0}); optionally forget the labels."""
+        self.slots[:, 0] = -1
+        self.slots[:, 1] = 0
+        if labels:
+            self.labels = []
+
+    def arm(self, lib, entity: str, worker: str, sweep: int):
+        i = len(self.labels)
+        if i >= self.slots.shape[0]:
+            raise ConfigError("launch trace full")
+        self.labels.append((entity, worker, sweep))
+        _lib.check(lib.edg_trace_next(_lib.ptr(self.slots[i])), "trace")
+
+    def records(self):
+        """[(entity, worker, sweep, start_ns, end_ns)] -- call after a synchronize."""
+        t = self.slots[:len(self.labels)].cpu().numpy().view(np.uint64)
+        return [(e, w, sw, int(t[i, 0]), int(t[i, 1])) for i, (e, w, sw) in enumerate(self.labels)]
+
+
 class _Base:
     def _common_alloc(self, max_steps):
         torch = self.torch
@@ -68,10 +124,20 @@ class _Base:
         self._graph_steps = 0
         self._graph_key = None
         self.kernel_timer = None      # optional KernelTimer (events around the hot kernels)
+        self.tracer = None            # optional LaunchTrace (per-launch device timestamps)
+
+    def _trace(self, entity):
+        """Arm the launch trace for the next launch (no-op without a tracer)."""
+        if self.tracer is not None:
+            self.tracer.arm(self.lib, entity, self._worker(), self.steps_done)
+
+    def _worker(self):
+        return "main"
 
     def _finalize_dt(self):
         """dt = cfl * min(candidates of the current state) (kernels.py:281);
         the device step counter status[2] indexes the dt history."""
+        self._trace("DtFinalize")
         _lib.check(self.lib.edg_dt_finalize(_lib.ptr(self.slots), float(self.cfl), _lib.ptr(self.dt),
                                             _lib.ptr(self.dt_hist), -self.max_steps, _lib.ptr(self.status),
                                             _stream()), "dt_finalize")
@@ -115,7 +181,11 @@ class _Base:
     def prepare_graph(self, chunk: int = 2):
         """Capture `chunk` steps into a CUDA graph (once).  The graph bakes in
         which physical buffer holds the state, so it is re-captured when an
-        odd number of eager steps has swapped the ping-pong roles."""
+        odd number of eager steps has swapped the ping-pong roles.  Captured
+        and instantiated through the C ABI (edg_graph_begin / edg_graph_end)
+        so that the kernel nodes keep the priorities of the streams they were
+        captured from (cudaGraphInstantiateFlagUseNodePriority): the
+        skeleton-first schedule survives the graph."""
         torch = self.torch
         if chunk % 2:
             raise ConfigError("graph chunk must be even (ping-pong buffers)")
@@ -124,13 +194,31 @@ class _Base:
             return
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
-        g = torch.cuda.CUDAGraph()
+        steps0 = self.steps_done
         with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
+            _lib.check(self.lib.edg_graph_begin(_stream()), "graph capture")
+            exc = None
+            try:
                 for _ in range(chunk):
                     self._enqueue_step()
+                    self.steps_done += 1
+            except BaseException as e:   # end the capture before re-raising
+                exc = e
+            ex = C.c_void_p()
+            prios = (C.c_int32 * 1024)()
+            nk = C.c_int32()
+            st = self.lib.edg_graph_end(_stream(), C.byref(ex), prios, 1024, C.byref(nk))
+            self.steps_done = steps0
+            if exc is not None:
+                if st == 0:
+                    self.lib.edg_graph_destroy(ex)
+                raise exc
+            _lib.check(st, "graph instantiate")
         torch.cuda.current_stream().wait_stream(side)
-        self._graph, self._graph_steps, self._graph_key = g, chunk, key
+        if self._graph is not None:
+            self._graph.close()
+        self._graph = _NativeGraph(self.lib, ex, list(prios[:min(nk.value, 1024)]))
+        self._graph_steps, self._graph_key = chunk, key
 
     def step(self):
         self._enqueue_step()
@@ -223,17 +311,28 @@ class DGSolver(_Base):
         return self.Q
 
     # ----------------------------------------------------------------- step --
-    def _stp(self, cell_list, nwork):
+    def _worker(self):
+        if self.adaptive and self.two_streams:
+            cur = self.torch.cuda.current_stream()
+            if cur == self.s_hi:
+                return "hi"
+            if cur == self.s_lo:
+                return "lo"
+        return "main"
+
+    def _stp(self, cell_list, nwork, entity="STP"):
+        self._trace(entity)
         return self.lib.edg_stp_picard(C.byref(self.native), self.order, _lib.ptr(self.table), _lib.ptr(self.Q),
                                        _lib.ptr(cell_list), nwork, _lib.ptr(self.edges), self.edges_per_cell,
                                        _lib.ptr(self.dt), self.tol, self.max_iter, _lib.ptr(self.q_end), None,
                                        _lib.ptr(self.trace_q), _lib.ptr(self.trace_f), _lib.ptr(self.iterations),
                                        _lib.ptr(self.converged), _lib.ptr(self.iter_total), _stream())
 
-    def _faces(self, off, cnt):
+    def _faces(self, off, cnt, entity="Faces"):
         """Rusanov on leaf faces [off, off + cnt) (skeleton-only faces come first)."""
         if cnt <= 0:
             return
+        self._trace(entity)
         sl = slice(off, off + cnt)
         _lib.check(self.lib.edg_faces_rusanov(C.byref(self.native), self.order, _lib.ptr(self.table), cnt,
                                               _lib.ptr(self.face_axis[sl]), _lib.ptr(self.face_cell[sl]),
@@ -242,6 +341,7 @@ class DGSolver(_Base):
                    "faces_rusanov")
 
     def _restrict(self):
+        self._trace("Restrict")
         _lib.check(self.lib.edg_faces_restrict(self.pde.dim, self.pde.m, self.order, _lib.ptr(self.table),
                                                self.mesh.nparent, _lib.ptr(self.parent_face),
                                                _lib.ptr(self.parent_children), _lib.ptr(self.face_cp),
@@ -259,6 +359,7 @@ class DGSolver(_Base):
             if tm:
                 tm.end("stp")
                 tm.begin("corrector")
+            self._trace("Corrector")
             _lib.check(lib.edg_corrector_grid(C.byref(self.native), self.order, _lib.ptr(self.table), self.mesh.N,
                                               int(self.mesh.periodic), _lib.ptr(self.q_end), _lib.ptr(self.trace_q),
                                               _lib.ptr(self.trace_f), _lib.ptr(self.edges), _lib.ptr(self.Qn),
@@ -272,21 +373,21 @@ class DGSolver(_Base):
             nsk, F = self.nface_sk, self.mesh.nleaf
 
             def skeleton_phase():
-                _lib.check(self._stp(self.skel, int(self.skel.numel())), "stp_picard(skeleton)")
-                self._faces(0, nsk)
+                _lib.check(self._stp(self.skel, int(self.skel.numel()), "SkeletonSTP"), "stp_picard(skeleton)")
+                self._faces(0, nsk, "SkeletonFaces")
                 self._restrict()
 
             def enclave_phase():
-                _lib.check(self._stp(self.encl, int(self.encl.numel())), "stp_picard(enclave)")
+                _lib.check(self._stp(self.encl, int(self.encl.numel()), "EnclaveSTP"), "stp_picard(enclave)")
 
             if tm is not None:
                 # timed (benchmark) order on one stream -- all predictors, then
                 # the faces: same results bitwise, the events bracket the kernels
                 tm.begin("stp")
-                _lib.check(self._stp(self.skel, int(self.skel.numel())), "stp_picard(skeleton)")
-                _lib.check(self._stp(self.encl, int(self.encl.numel())), "stp_picard(enclave)")
+                _lib.check(self._stp(self.skel, int(self.skel.numel()), "SkeletonSTP"), "stp_picard(skeleton)")
+                _lib.check(self._stp(self.encl, int(self.encl.numel()), "EnclaveSTP"), "stp_picard(enclave)")
                 tm.end("stp")
-                self._faces(0, nsk)
+                self._faces(0, nsk, "SkeletonFaces")
                 self._restrict()
             elif self.two_streams:
                 main = torch.cuda.current_stream()
@@ -304,6 +405,7 @@ class DGSolver(_Base):
             self._faces(nsk, F - nsk)
             if tm:
                 tm.begin("corrector")
+            self._trace("Corrector")
             _lib.check(lib.edg_corrector(C.byref(self.native), self.order, _lib.ptr(self.table), self.ncells,
                                          _lib.ptr(self.q_end), _lib.ptr(self.trace_q), _lib.ptr(self.trace_f),
                                          None, _lib.ptr(self.side_face), _lib.ptr(self.outcomes),
@@ -361,6 +463,7 @@ class FVSolver(_Base):
         tm = self.kernel_timer
         if tm:
             tm.begin("fv")
+        self._trace("FVPatch")
         _lib.check(lib.edg_fv_grid_step(C.byref(self.native), self.k, self.pmesh.N, int(self.pmesh.periodic),
                                         _lib.ptr(self.Q), _lib.ptr(self.dt), _lib.ptr(self.edges),
                                         _lib.ptr(self.Qn), _lib.ptr(self.slots), self.h_cell,

@@ -1,113 +1,59 @@
-"""The kernel variants selected by environment switches (read once per
-process by the library) run the same parity cases as the defaults, each in a
-subprocess:
+"""The two fused Riemann + corrector kernels agree bit for bit.
 
-* EDG_STP_PEN=1   pencil-formulation 2-D STP (edg_stp_pen.cuh) and
-  EDG_STP_PAIR=1  node-pair / time-split 2-D STP (edg_stp_pair.cuh): the cfg2
-                  9x9 reference trajectory (CFL 0.2) within 1e-10 and
-                  identical Picard counts;
-* EDG_CORR_PIPE=0 one-CTA-per-group corrector against the pipelined one
-                  (EDG_CORR_PIPE=1) on 2-D and 3-D grids, and EDG_CORR_PIPE=1 the pipelined one
-                  on the adaptive cfg5 mesh: bitwise equal to the defaults;
-* EDG_FV_PIPE=1   persistent FV grid kernel: bitwise equal (16^3 volumes, 5 steps).
+The uniform-grid step uses the persistent, bulk-copy double-buffered
+corrector (`corrector_grid_pipe_kernel`, edg_corr_pipe.cuh) whenever the grid
+gives a persistent CTA more than one group of cells; smaller grids and the
+neighbour-table entry point (`edg_corrector` with `nbr`) use the
+one-CTA-per-group kernel (`corrector_kernel<..., FUSED>`, edg_faces.cuh).  Both
+restate kernels.py:162-193 with the same operation order, so on the same
+predictor output they must give identical bits, including the next step's dt
+candidates.  The grids below are large enough for the pipelined kernel.
 """
-import os
-import subprocess
-import sys
-
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
-REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-_RUN = r"""
-import sys, numpy as np
-sys.path.insert(0, {repo!r})
-import paper_1806_07984_b200 as edg
-kind = {kind!r}
-g = np.load({golden!r})
-if kind == "dg":
-    tag = {tag!r}
-    N, dim, p, periodic, steps, cells, wlo = (int(v) for v in g[tag + "_meta"])
-    base = {{"cfg2s": "cfg2", "cfg3w": "cfg3"}}[tag]
-    cfg = edg.configs.CONFIGS[base].with_(cfl=float(g[tag + "_cfl"]))
+
+def _predict(cfg, N):
+    import paper_1806_07984_b200 as edg
+    cfg = cfg.with_(cells=N)
     pde = edg.pde.make_pde(cfg.pde, dim=cfg.dim)
-    mesh = edg.mesh.CartesianMesh(N, cfg.dim, bool(periodic), extent=N / cells)
+    mesh = edg.mesh.CartesianMesh(N, cfg.dim, cfg.periodic)
     s = edg.solver.DGSolver(pde, cfg.order, mesh, cfg.cfl)
-    s.set_state(g[tag + "_q0"])
-    s.run(steps, graph=False)
-    s.check_status()
-    np.savez({out!r}, q=s.state().cpu().numpy(), its=s.iterations.cpu().numpy(), dt=s.dt_history())
-elif kind == "amr":
-    cfg = edg.configs.CONFIGS["cfg5"].with_(cells=27)
-    mesh = edg.mesh.AdaptiveMesh(edg.configs.amr_cells(cfg), 2, True)
-    s = edg.solver.DGSolver(edg.pde.euler(2), cfg.order, mesh, cfg.cfl)
-    s.set_state(edg.configs.initial_dg_amr(cfg, mesh.cells))
-    s.run(4, graph=False)
-    s.check_status()
-    np.savez({out!r}, q=s.state().cpu().numpy(), its=s.iterations.cpu().numpy(), dt=s.dt_history())
-else:
-    cfg = edg.configs.CONFIGS["cfg4"]
-    s = edg.solver.FVSolver(edg.pde.euler(3), 16, 8, cfg.cfl)
-    s.set_state(g["cfg4p_q0"])
-    s.run(5, graph=False)
-    s.check_status()
-    np.savez({out!r}, q=s.state().cpu().numpy(), its=np.zeros(1), dt=s.dt_history())
-"""
+    s.set_state(edg.configs.initial_dg_uniform(cfg))
+    s._finalize_dt()
+    edg._lib.check(s._stp(s.work_order, s.ncells), "stp")
+    return edg, s
 
 
-def _run(tmp_path, env_kv, kind, tag=""):
-    out = str(tmp_path / f"{kind}_{tag}_{'_'.join(f'{k}{v}' for k, v in env_kv.items()) or 'default'}.npz")
-    code = _RUN.format(repo=REPO, kind=kind, tag=tag, out=out,
-                       golden=os.path.join(REPO, "tests", "golden", "traj.npz"))
-    env = dict(os.environ)
-    for k in ("EDG_STP_PEN", "EDG_STP_PAIR", "EDG_CORR_PIPE", "EDG_FV_PIPE"):
-        env.pop(k, None)
-    env.update(env_kv)
-    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stderr[-3000:]
-    return np.load(out)
+@pytest.mark.parametrize("name,N", [("cfg2", 128), ("cfg3", 20)])
+def test_pipelined_corrector_equals_one_cta_per_group(name, N):
+    import ctypes as C
+    import torch
+    edg, s = _predict(edg_cfg(name), N)
+    lib = s.lib
+    slots_a = torch.empty_like(s.slots)
+    slots_b = torch.empty_like(s.slots)
+    status = torch.zeros_like(s.status)
+    for sl in (slots_a, slots_b):
+        edg._lib.check(lib.edg_dt_slots_reset(edg._lib.ptr(sl), edg.kernels._stream()), "reset")
+    # pipelined grid kernel (solver path)
+    out_a = torch.empty_like(s.Q)
+    edg._lib.check(lib.edg_corrector_grid(C.byref(s.native), s.order, edg._lib.ptr(s.table), s.mesh.N,
+                                          int(s.mesh.periodic), edg._lib.ptr(s.q_end), edg._lib.ptr(s.trace_q),
+                                          edg._lib.ptr(s.trace_f), edg._lib.ptr(s.edges), edg._lib.ptr(out_a),
+                                          edg._lib.ptr(slots_a), edg._lib.ptr(s.hmin), edg._lib.ptr(status),
+                                          edg.kernels._stream()), "grid corrector")
+    # one-CTA-per-group kernel through the neighbour table
+    out_b = edg.kernels.corrector_batch(s.pde, s.basis, s.q_end, s.trace_f, [s.mesh.h] * s.pde.dim, nbr=s.nbr,
+                                        trace_q=s.trace_q, dt_slots=slots_b, hmin=s.hmin, status=status)
+    torch.cuda.synchronize()
+    assert torch.equal(out_a, out_b)
+    assert torch.equal(slots_a, slots_b)
+    assert int(status[0].item()) == 0
 
 
-@pytest.mark.parametrize("env", [{"EDG_STP_PAIR": "1"}])
-def test_pair_stp_vs_reference(tmp_path, env):
-    """Node-pair / time-split 2-D predictor (edg_stp_pair.cuh)."""
-    g = np.load(os.path.join(REPO, "tests", "golden", "traj.npz"))
-    r = _run(tmp_path, env, "dg", "cfg2s")
-    q = g["cfg2s_q"]
-    assert np.max(np.abs(r["q"] - q)) / np.max(np.abs(q)) <= 1e-10
-    assert np.array_equal(r["its"], g["cfg2s_its"][-1])
-
-
-def test_pencil_stp_vs_reference(tmp_path):
-    g = np.load(os.path.join(REPO, "tests", "golden", "traj.npz"))
-    r = _run(tmp_path, {"EDG_STP_PEN": "1"}, "dg", "cfg2s")
-    q = g["cfg2s_q"]
-    assert np.max(np.abs(r["q"] - q)) / np.max(np.abs(q)) <= 1e-10
-    assert np.array_equal(r["its"], g["cfg2s_its"][-1])
-
-
-@pytest.mark.parametrize("tag,env", [("cfg2s", {"EDG_CORR_PIPE": "0"}), ("cfg3w", {"EDG_CORR_PIPE": "0"})])
-def test_corrector_variants_bitwise(tmp_path, tag, env):
-    # the small test grids give every persistent CTA at most one group, so the
-    # automatic choice would take the one-CTA-per-group kernel: force the
-    # pipelined one (EDG_CORR_PIPE=1) against it
-    a = _run(tmp_path, {"EDG_CORR_PIPE": "1"}, "dg", tag)
-    b = _run(tmp_path, env, "dg", tag)
-    assert np.array_equal(a["q"], b["q"])
-    assert np.array_equal(a["dt"], b["dt"])
-
-
-def test_adaptive_corrector_variant_bitwise(tmp_path):
-    a = _run(tmp_path, {}, "amr")
-    b = _run(tmp_path, {"EDG_CORR_PIPE": "1"}, "amr")
-    assert np.array_equal(a["q"], b["q"])
-    assert np.array_equal(a["dt"], b["dt"])
-
-
-def test_fv_pipe_bitwise(tmp_path):
-    a = _run(tmp_path, {}, "fv")
-    b = _run(tmp_path, {"EDG_FV_PIPE": "1"}, "fv")
-    assert np.array_equal(a["q"], b["q"])
-    assert np.array_equal(a["dt"], b["dt"])
+def edg_cfg(name):
+    import paper_1806_07984_b200 as edg
+    return edg.configs.CONFIGS[name]
