@@ -539,6 +539,9 @@ def run_ours(args, cfg):
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(r["solver"], r["Q0"], r["dof"], args.steps, ws, dist, dev)
+    schedule = None
+    if cfg.kind == "dg-amr":
+        schedule = measure_schedule(cfg, args.steps, args.warmup)
     secondary = None
     if cfg.name == "cfg3" and not args.no_secondary:
         secondary = measure_secondary(ws, dist, dev, peak64, local)
@@ -576,10 +579,65 @@ def run_ours(args, cfg):
             "cpu_baseline": cpu,
             "parity_safe_variant": variant,
             "secondary": secondary,
+            "schedule": schedule,
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def measure_schedule(cfg, steps, warmup):
+    """Config 5's schedule: CUDA-graph replay of the two-priority-stream step
+    (the production path) against the same steps on one stream, and the
+    launch trace of one replayed two-step graph (solver.LaunchTrace): the
+    skeleton predictor's head start over the enclave predictor and the
+    slack between the end of the skeleton phase (faces + restriction) and the
+    end of the enclave predictor (positive = fully hidden)."""
+    import torch
+    from paper_1806_07984_b200 import solver as S
+    out = {}
+    flush = l2_flush_buffer(cfg)
+    for two in (True, False):
+        s, Q0, _ = build_solver(cfg)
+        if not two:
+            s = S.DGSolver(s.pde, s.order, s.mesh, s.cfl, check_finite=False, two_streams=False)
+        s.set_state(Q0)
+        s.run(warmup + warmup % 2, graph=True)
+        s.set_state(Q0)
+        s.prepare_graph(2)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        total = 0.0
+        for _ in range(max(1, steps // 2)):
+            if flush is not None:
+                flush.zero_()
+            a.record()
+            s.run(2, graph=True)
+            b.record()
+            torch.cuda.synchronize()
+            total += a.elapsed_time(b)
+        out["two_streams_ms_per_step" if two else "one_stream_ms_per_step"] = total / (2 * max(1, steps // 2))
+        if two:
+            s.tracer = S.LaunchTrace()
+            s._graph = None
+            s.prepare_graph(2)
+            heads, slack = [], []
+            for _ in range(5):
+                s.tracer.reset()
+                s._graph.replay()
+                torch.cuda.synchronize()
+                ph = {}
+                for ent, _w, sw, t0, t1 in s.tracer.records():
+                    ph.setdefault(sw, {})[ent] = (t0, t1)
+                for p in ph.values():
+                    heads.append((p["EnclaveSTP"][0] - p["SkeletonSTP"][0]) * 1e-3)
+                    slack.append((p["EnclaveSTP"][1] - p["Restrict"][1]) * 1e-3)
+            out["skeleton_stp_head_start_us"] = {"min": min(heads), "median": statistics.median(heads)}
+            out["skeleton_phase_slack_us"] = {"min": min(slack), "median": statistics.median(slack)}
+            s.tracer = None
+        del s
+    out["two_stream_speedup"] = out["one_stream_ms_per_step"] / out["two_streams_ms_per_step"]
+    return out
 
 
 def measure_secondary(ws, dist, dev, peak64, local):

@@ -82,6 +82,18 @@ int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev,
                    double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev,
                    unsigned long long* iter_total_dev, void* stream);
 
+/* Same contract as edg_stp_picard, launched for a background (low-priority)
+ * stream: one work block per CTA instead of persistent CTAs, so the CTAs
+ * retire as they finish and the high-priority skeleton work of the schedule
+ * gets SM slots while this launch is still running. */
+int edg_stp_picard_background(const edg_pde* pde, int32_t order, const double* basis_dev,
+                   const double* q_dev, const int32_t* cell_list_dev, int32_t nwork,
+                   const double* edges_dev, int32_t edges_per_cell, const double* dt_dev,
+                   double tol, int32_t max_iter,
+                   double* q_end_dev, double* q_int_dev, double* trace_q_dev,
+                   double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev,
+                   unsigned long long* iter_total_dev, void* stream);
+
 /* ---- stp_linear (kernels.py:82-106): Cauchy-Kowalevski predictor of a
  * linear PDE (advection); other PDEs -> EDG_ERR_NO_SPEED (EnclaveDgError
  * "stp_linear requires a linear flux").  Same buffers as edg_stp_picard;
@@ -265,6 +277,16 @@ int edg_pack_face_traces(int32_t nsides, int32_t row_len, int32_t nfaces, const 
                          double* out_dev, void* stream);
 int edg_unpack_face_traces(int32_t row_len, int32_t nfaces, const int32_t* slot_dev, const double* in_dev,
                            double* ghost_dev, void* stream);
+/* Row gather / scatter of the sharded step (paper_1806_07984_b200/sharded.py;
+ * the send_face / receive_face payload placement of SPEC.md:447-466):
+ * gather  dst[j] = src[idx[j]]  (pack: rows of trace_q viewed as
+ *          (cells * 2d, m * n^(d-1)), idx = cell * 2d + side slot);
+ * scatter dst[idx[j]] = src[j]  (unpack into the ghost rows).
+ * Rows are row_len doubles; idx is int64. */
+int edg_gather_rows(int32_t row_len, int32_t nrows, const int64_t* idx_dev, const double* src_dev, double* dst_dev,
+                    void* stream);
+int edg_scatter_rows(int32_t row_len, int32_t nrows, const int64_t* idx_dev, const double* src_dev, double* dst_dev,
+                     void* stream);
 
 #ifdef __cplusplus
 }

@@ -8,6 +8,6 @@ the Algorithm-1 loop and the enclave task runtime with a two-priority-stream
 CUDA schedule.  All compute runs in libenclavedg_b200.so (hand-written fp64
 CUDA for sm_100a) through the C ABI in include/enclavedg_b200.h.
 """
-from . import errors, configs, basis, pde, _lib, kernels, transfer, mesh, solver, decomposition  # noqa: F401
+from . import errors, configs, basis, pde, _lib, kernels, transfer, mesh, solver, decomposition, sharded, io  # noqa: F401
 
-__all__ = ["errors", "configs", "basis", "pde", "kernels", "transfer", "mesh", "solver", "decomposition"]
+__all__ = ["errors", "configs", "basis", "pde", "kernels", "transfer", "mesh", "solver", "decomposition", "sharded", "io"]

@@ -36,6 +36,7 @@ SIGNATURES = {
     "edg_build_info": (C.c_char_p, []),
     "edg_last_error": (C.c_char_p, []),
     "edg_stp_picard": (C.c_int, [PDEP, I32, P, P, P, I32, P, I32, P, D, I32, P, P, P, P, P, P, P, P]),
+    "edg_stp_picard_background": (C.c_int, [PDEP, I32, P, P, P, I32, P, I32, P, D, I32, P, P, P, P, P, P, P, P]),
     "edg_stp_linear": (C.c_int, [PDEP, I32, P, P, P, I32, P, I32, P, P, P, P, P, P, P, P]),
     "edg_probe_fp64": (C.c_int, [P, I32, I32, P]),
     "edg_probe_dmma": (C.c_int, [P, I32, I32, P]),
@@ -65,6 +66,8 @@ SIGNATURES = {
     "edg_restrict_volume": (C.c_int, [I32, I32, I32, P, I32, P, P, P]),
     "edg_pack_face_traces": (C.c_int, [I32, I32, I32, P, P, P, P, P, P]),
     "edg_unpack_face_traces": (C.c_int, [I32, I32, P, P, P, P]),
+    "edg_gather_rows": (C.c_int, [I32, I32, P, P, P, P]),
+    "edg_scatter_rows": (C.c_int, [I32, I32, P, P, P, P]),
 }
 
 _LIB = None

@@ -104,7 +104,9 @@ int edg_supported(const edg_pde* pde, int32_t order) {
   return order >= 1 && order + 1 <= u->max_n();
 }
 
-int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev, const double* q_dev,
+}  // extern "C"
+
+static int stp_picard_launch(int ctas_per_sm, const edg_pde* pde, int32_t order, const double* basis_dev, const double* q_dev,
                    const int32_t* cell_list_dev, int32_t nwork, const double* edges_dev, int32_t edges_per_cell,
                    const double* dt_dev, double tol, int32_t max_iter, double* q_end_dev, double* q_int_dev,
                    double* trace_q_dev, double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev,
@@ -137,7 +139,34 @@ int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev, c
   a.converged = converged_dev;
   a.iter_total = iter_total_dev;
   a.trace = trace;
+  a.ctas_per_sm = ctas_per_sm;
   return cuda_status(u->stp(order + 1, a, (cudaStream_t)stream));
+}
+
+extern "C" {
+
+int edg_stp_picard(const edg_pde* pde, int32_t order, const double* basis_dev, const double* q_dev,
+                   const int32_t* cell_list_dev, int32_t nwork, const double* edges_dev, int32_t edges_per_cell,
+                   const double* dt_dev, double tol, int32_t max_iter, double* q_end_dev, double* q_int_dev,
+                   double* trace_q_dev, double* trace_f_dev, int32_t* iterations_dev, uint8_t* converged_dev,
+                   unsigned long long* iter_total_dev, void* stream) {
+  return stp_picard_launch(0, pde, order, basis_dev, q_dev, cell_list_dev, nwork, edges_dev, edges_per_cell, dt_dev,
+                           tol, max_iter, q_end_dev, q_int_dev, trace_q_dev, trace_f_dev, iterations_dev,
+                           converged_dev, iter_total_dev, stream);
+}
+
+#ifndef EDG_STP_BACKGROUND_CTAS
+#define EDG_STP_BACKGROUND_CTAS (-1)
+#endif
+int edg_stp_picard_background(const edg_pde* pde, int32_t order, const double* basis_dev, const double* q_dev,
+                              const int32_t* cell_list_dev, int32_t nwork, const double* edges_dev,
+                              int32_t edges_per_cell, const double* dt_dev, double tol, int32_t max_iter,
+                              double* q_end_dev, double* q_int_dev, double* trace_q_dev, double* trace_f_dev,
+                              int32_t* iterations_dev, uint8_t* converged_dev, unsigned long long* iter_total_dev,
+                              void* stream) {
+  return stp_picard_launch(EDG_STP_BACKGROUND_CTAS, pde, order, basis_dev, q_dev, cell_list_dev, nwork, edges_dev,
+                           edges_per_cell, dt_dev, tol, max_iter, q_end_dev, q_int_dev, trace_q_dev, trace_f_dev,
+                           iterations_dev, converged_dev, iter_total_dev, stream);
 }
 
 int edg_stp_linear(const edg_pde* pde, int32_t order, const double* basis_dev, const double* q_dev,
@@ -736,6 +765,20 @@ __global__ void unpack_face_traces_kernel(int row_len, int nfaces, const int32_t
 static unsigned copy_blocks(int rows) {
   return (unsigned)(rows < 148 * 16 ? rows : 148 * 16);   // 16 CTAs of 128 threads per SM
 }
+
+// Row gather / scatter of the sharded step (sharded.py): one warp per row of
+// row_len doubles (a face trace: m * n^(d-1) = 24..125 doubles), 8 warps per CTA.
+template <bool SCATTER>
+__global__ void __launch_bounds__(256) rows_copy_kernel(int row_len, int nrows, const int64_t* __restrict__ idx,
+                                                        const double* __restrict__ src, double* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < nrows; r += gridDim.x * 8) {
+    const long long o = __ldg(idx + r) * row_len, p = (long long)r * row_len;
+    const double* s = src + (SCATTER ? p : o);
+    double* d = dst + (SCATTER ? o : p);
+    for (int e = lane; e < row_len; e += 32) d[e] = __ldg(s + e);
+  }
+}
 }  // namespace edg
 
 extern "C" {
@@ -747,6 +790,28 @@ int edg_pack_face_traces(int32_t nsides, int32_t row_len, int32_t nfaces, const 
   if (nfaces == 0) return EDG_OK;
   pack_face_traces_kernel<<<copy_blocks(2 * nfaces), 128, 0, (cudaStream_t)stream>>>(
       nsides, row_len, nfaces, cell_dev, side_dev, trace_q_dev, trace_f_dev, out_dev);
+  return cuda_status(check_launch());
+}
+
+int edg_gather_rows(int32_t row_len, int32_t nrows, const int64_t* idx_dev, const double* src_dev, double* dst_dev,
+                    void* stream) {
+  if (row_len < 1 || nrows < 0) return fail(EDG_ERR_CONFIG, "bad gather shape");
+  if (nrows == 0) return EDG_OK;
+  if (!idx_dev || !src_dev || !dst_dev) return fail(EDG_ERR_CONFIG, "null buffer");
+  const int blocks = (nrows + 7) / 8;
+  rows_copy_kernel<false><<<blocks < 148 * 8 ? blocks : 148 * 8, 256, 0, (cudaStream_t)stream>>>(row_len, nrows, idx_dev,
+                                                                                              src_dev, dst_dev);
+  return cuda_status(check_launch());
+}
+
+int edg_scatter_rows(int32_t row_len, int32_t nrows, const int64_t* idx_dev, const double* src_dev, double* dst_dev,
+                     void* stream) {
+  if (row_len < 1 || nrows < 0) return fail(EDG_ERR_CONFIG, "bad scatter shape");
+  if (nrows == 0) return EDG_OK;
+  if (!idx_dev || !src_dev || !dst_dev) return fail(EDG_ERR_CONFIG, "null buffer");
+  const int blocks = (nrows + 7) / 8;
+  rows_copy_kernel<true><<<blocks < 148 * 8 ? blocks : 148 * 8, 256, 0, (cudaStream_t)stream>>>(row_len, nrows, idx_dev,
+                                                                                             src_dev, dst_dev);
   return cuda_status(check_launch());
 }
 

@@ -220,7 +220,10 @@ __device__ __forceinline__ double from_maxkey(unsigned long long k) {
   return k == 0xFFFFFFFFFFFFFFFFull ? __longlong_as_double(0x7FF8000000000000ll) : __longlong_as_double((long long)k);
 }
 
-constexpr unsigned long long DT_EMPTY = 0xFFFFFFFFFFFFFFFFull;   // no candidate yet
+// no candidate yet: above every positive double's bits (+inf is 0x7FF0...) as
+// an unsigned AND as a signed 64-bit integer, so the slots of several ranks can
+// be combined with an int64 MIN all-reduce (decomposition.global_dt_slots)
+constexpr unsigned long long DT_EMPTY = 0x7FFFFFFFFFFFFFFFull;
 
 // Max of `key` over the lanes of this warp that share `seg` (segments are
 // contiguous lane ranges, e.g. the nodes of one cell), then one shared-memory

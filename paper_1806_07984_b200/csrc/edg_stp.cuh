@@ -45,6 +45,11 @@ struct StpArgs {
   uint8_t* converged;
   unsigned long long* iter_total;   // optional: += sum of per-cell iterations
   unsigned long long* trace;        // optional launch-trace slot (TraceScope)
+  // grid policy: 0 = persistent CTAs at full occupancy; > 0 = persistent, at
+  // most that many CTAs per SM; < 0 = one work block per CTA, so the CTAs
+  // retire as they finish and launches on higher-priority streams get their
+  // slots (the enclave predictor of the two-stream schedule)
+  int32_t ctas_per_sm;
 };
 
 constexpr int stp_best_cpb(int npc, int target) {

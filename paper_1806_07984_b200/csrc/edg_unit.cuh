@@ -92,9 +92,18 @@ static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
     if (upload_ops<N>(a.basis, st)) return EDG_ERR_CUDA;
   }
   const int blocks = (a.nwork + Cf::CPB - 1) / Cf::CPB;
-  // persistent CTAs (the kernel strides over work blocks)
-  const int cap = persistent_grid(kern, Cf::THREADS, smem);
+  // persistent CTAs (the kernel strides over work blocks), capped per SM or
+  // one block per CTA as the launch's grid policy asks
+  int cap = persistent_grid(kern, Cf::THREADS, smem);
   if (cap < 0) return EDG_ERR_CUDA;
+  if (a.ctas_per_sm < 0) {
+    cap = blocks;
+  } else if (a.ctas_per_sm > 0) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return EDG_ERR_CUDA;
+    if (sms * a.ctas_per_sm < cap) cap = sms * a.ctas_per_sm;
+  }
   const int grid = blocks < cap ? blocks : cap;
   if (grid > 0) kern<<<grid, Cf::THREADS, smem, st>>>(a);
   return check_launch();

@@ -40,14 +40,20 @@ def _morton3_key(idx, depth):
     return tuple(tuple((i // 3 ** (depth - l)) % 3 for i in idx) for l in range(1, depth + 1))
 
 
+def _depth(N):
+    """Tree depth of an N-per-axis uniform mesh (N = 3^depth for the reference's meshes)."""
+    depth = 1
+    while 3 ** depth < N:
+        depth += 1
+    return depth
+
+
 def sfc_order(mesh):
     """Cell indices of `mesh` in space-filling-curve order."""
     if isinstance(mesh, AdaptiveMesh):
         return np.arange(mesh.ncells, dtype=np.int64)   # cells are stored in SFC order
     if isinstance(mesh, CartesianMesh):
-        depth = 1
-        while 3 ** depth < mesh.N:
-            depth += 1
+        depth = _depth(mesh.N)
         keys = [_morton3_key(tuple(int(v) for v in row), depth) for row in mesh.index]
         return np.array(sorted(range(mesh.ncells), key=keys.__getitem__), dtype=np.int64)
     raise ConfigError(f"unsupported mesh type {type(mesh).__name__}")
@@ -64,13 +70,16 @@ def interior_faces(mesh):
         keys = [(k[1], k[2], k[3]) for k, ok in zip(mesh._leaf_keys, keep) if ok]
         return mesh.face_cell[keep].astype(np.int64), keys
     if isinstance(mesh, CartesianMesh):
+        # FaceRecord.key of the reference uniform mesh: (axis, level, index of
+        # the upper cell), which wraps to 0 along the axis on a periodic face
+        depth = _depth(mesh.N)
         out, keys = [], []
         for a in range(mesh.dim):
             hi = mesh.nbr[:, 2 * a + 1].astype(np.int64)
             lo = np.arange(mesh.ncells, dtype=np.int64)
             ok = (hi >= 0) & (hi != lo)
             out.append(np.stack([lo[ok], hi[ok]], axis=1))
-            keys.extend((a, 0, int(c)) for c in lo[ok])
+            keys.extend((a, depth, tuple(int(v) for v in mesh.index[c])) for c in hi[ok])
         return np.concatenate(out, axis=0), keys
     raise ConfigError(f"unsupported mesh type {type(mesh).__name__}")
 
@@ -181,6 +190,13 @@ def pack_boundary_traces(plan: ExchangePlan, peer: int, trace_q, trace_f):
     import torch
     from . import _lib
     from .kernels import _stream
+    for t, nm in ((trace_q, "trace_q"), (trace_f, "trace_f")):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ConfigError(f"{nm} must be a contiguous float64 CUDA tensor")
+    if trace_q.shape != trace_f.shape or trace_q.device != trace_f.device or trace_q.dim() < 3:
+        raise ConfigError("trace_q and trace_f must have the same (C, 2d, m, ...) shape on one device")
+    if peer not in plan.local_cell:
+        raise ConfigError(f"rank {peer} is not a neighbour of rank {plan.rank}")
     C_, nsides = trace_q.shape[0], trace_q.shape[1]
     row_len = trace_q[0, 0].numel()
     dev = trace_q.device
@@ -202,10 +218,20 @@ def unpack_boundary_traces(recv, slots, ghost):
     import torch
     from . import _lib
     from .kernels import _stream
-    if isinstance(slots, torch.Tensor) and slots.dtype == torch.int32 and slots.device == ghost.device:
-        slot = slots                     # already resident: no per-step upload
+    for t, nm in ((recv, "recv"), (ghost, "ghost")):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ConfigError(f"{nm} must be a contiguous float64 CUDA tensor")
+    if recv.dim() != 3 or ghost.dim() != 3 or recv.shape[1] != 2 or ghost.shape[1] != 2 or \
+            recv.shape[2] != ghost.shape[2] or recv.device != ghost.device:
+        raise ConfigError(f"recv {tuple(recv.shape)} / ghost {tuple(ghost.shape)}: expected (k, 2, L) / (G, 2, L)")
+    if isinstance(slots, torch.Tensor):
+        slot = slots.to(device=ghost.device, dtype=torch.int32).contiguous()
     else:
         slot = torch.as_tensor(np.asarray(slots, dtype=np.int32)).to(ghost.device)
+    if slot.numel() != recv.shape[0]:
+        raise ConfigError(f"{slot.numel()} slots for {recv.shape[0]} received rows")
+    if slot.numel() and (int(slot.min()) < 0 or int(slot.max()) >= ghost.shape[0]):
+        raise ConfigError(f"ghost slot outside [0, {ghost.shape[0]})")
     _lib.check(_lib.load().edg_unpack_face_traces(recv.shape[-1], recv.shape[0], _lib.ptr(slot), _lib.ptr(recv),
                                                   _lib.ptr(ghost), _stream()), "unpack face traces")
     return ghost
@@ -235,11 +261,26 @@ def exchange_traces(dist, plan: ExchangePlan, send: dict):
     return recv
 
 
-def global_dt(dist, local_dt):
-    """Admissible dt of the whole domain: all-reduce MIN of the per-rank dt
-    (the device reduction `edg_dt_finalize` yields the per-rank value)."""
+def global_dt(dist, local_candidate, cfl=1.0):
+    """Admissible dt of the whole domain (kernels.py:267-281 over all ranks):
+    all-reduce MIN of each rank's raw candidate min_c h_c / ((2p+1) lambda_c)
+    -- None or +inf for a rank without a positive wave speed -- THEN the cfl
+    factor, so the result is bitwise the single-domain one and a quiet rank
+    cannot poison it.  Raises EnclaveDgError only when no rank has a
+    candidate.  The reduction tensor lives on the backend's device (CUDA for
+    NCCL).  The device path of the sharded step all-reduces the 256 dt slots
+    instead (sharded.ShardedDGSolver)."""
     import torch
-    t = local_dt if isinstance(local_dt, torch.Tensor) else torch.tensor([float(local_dt)], dtype=torch.float64)
-    t = t.reshape(1).clone()
+    from .errors import EnclaveDgError
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    if isinstance(local_candidate, torch.Tensor):
+        t = local_candidate.detach().to(device=dev, dtype=torch.float64).reshape(1).clone()
+    else:
+        v = float("inf") if local_candidate is None else float(local_candidate)
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+    t = torch.where(torch.isnan(t) | (t <= 0), torch.full_like(t, float("inf")), t)
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
-    return t
+    best = float(t.item())
+    if best == float("inf"):
+        raise EnclaveDgError("no positive wave speed anywhere; cannot pick a time step")
+    return float(cfl) * best

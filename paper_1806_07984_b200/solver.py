@@ -320,9 +320,10 @@ class DGSolver(_Base):
                 return "lo"
         return "main"
 
-    def _stp(self, cell_list, nwork, entity="STP"):
+    def _stp(self, cell_list, nwork, entity="STP", background=False):
         self._trace(entity)
-        return self.lib.edg_stp_picard(C.byref(self.native), self.order, _lib.ptr(self.table), _lib.ptr(self.Q),
+        fn = self.lib.edg_stp_picard_background if background else self.lib.edg_stp_picard
+        return fn(C.byref(self.native), self.order, _lib.ptr(self.table), _lib.ptr(self.Q),
                                        _lib.ptr(cell_list), nwork, _lib.ptr(self.edges), self.edges_per_cell,
                                        _lib.ptr(self.dt), self.tol, self.max_iter, _lib.ptr(self.q_end), None,
                                        _lib.ptr(self.trace_q), _lib.ptr(self.trace_f), _lib.ptr(self.iterations),
@@ -377,8 +378,9 @@ class DGSolver(_Base):
                 self._faces(0, nsk, "SkeletonFaces")
                 self._restrict()
 
-            def enclave_phase():
-                _lib.check(self._stp(self.encl, int(self.encl.numel()), "EnclaveSTP"), "stp_picard(enclave)")
+            def enclave_phase(background=False):
+                _lib.check(self._stp(self.encl, int(self.encl.numel()), "EnclaveSTP", background),
+                           "stp_picard(enclave)")
 
             if tm is not None:
                 # timed (benchmark) order on one stream -- all predictors, then
@@ -396,7 +398,7 @@ class DGSolver(_Base):
                 with torch.cuda.stream(self.s_hi):
                     skeleton_phase()
                 with torch.cuda.stream(self.s_lo):
-                    enclave_phase()
+                    enclave_phase(background=True)
                 main.wait_stream(self.s_hi)
                 main.wait_stream(self.s_lo)
             else:

@@ -4,8 +4,8 @@ Run in the build container (the only place /root/reference exists):
 
     python tests/golden/make_golden_decomp.py
 
-For a uniform 9x9 periodic mesh and the same mesh with a refined block, and
-R in {2, 3, 4}, the decomposition is the contiguous SFC split of the
+For uniform 3x3 (R in {2, 3, 4, 5}) and 9x9 periodic meshes and the 9x9 mesh
+with a refined block (R in {2, 3, 4}), the decomposition is the contiguous SFC split of the
 reference's own `mesh.sfc_cells` (SPEC.md rank-sim `decompose`); recorded are
 the reference's `boundary_face_order(mesh, decomp, pair)` (mesh.py:613-628)
 as (lo key, hi key, face key) triples in order, and the skeleton set of
@@ -55,6 +55,9 @@ def _record(mesh, R):
 
 def main():
     out = {}
+    m3 = rm.build_uniform(1, dim=2, periodic=True)
+    out["uniform3"] = dict(cells=[list(n.key) for n in m3.sfc_cells],
+                           cases=[_record(m3, R) for R in (2, 3, 4, 5)])
     mesh = rm.build_uniform(2, dim=2, periodic=True)
     out["uniform9"] = dict(cells=[list(n.key) for n in mesh.sfc_cells],
                            cases=[_record(mesh, R) for R in (2, 3, 4)])

@@ -22,7 +22,31 @@ def _key(k):
     return tuple(tuple(x) if isinstance(x, list) else x for x in k)
 
 
-@pytest.mark.parametrize("name", ["uniform9", "refined"])
+@pytest.mark.parametrize("name,N", [("uniform3", 3), ("uniform9", 9)])
+def test_cartesian_against_reference_mesh(name, N):
+    """A periodic CartesianMesh decomposes like the reference's uniform mesh:
+    same partition, same boundary faces in the same order (face keys
+    (axis, level, upper cell index) with the periodic wrap), same skeleton."""
+    G = GOLDEN[name]
+    mesh = CartesianMesh(N, 2, True)
+    level = G["cells"][0][0]
+    key_of = {(level, tuple(int(v) for v in mesh.index[c])): c for c in range(mesh.ncells)}
+    faces, fkeys = interior_faces(mesh)
+    for case in G["cases"]:
+        R = case["R"]
+        dec = decompose(mesh, R)
+        for pair, want in case["pairs"].items():
+            r1, r2 = map(int, pair.split(","))
+            got = boundary_face_order(mesh, dec, (r1, r2))
+            assert list(got) == list(boundary_face_order(mesh, dec, (r2, r1)))
+            got_t = [(faces[f, 0], faces[f, 1], fkeys[f]) for f in got]
+            want_t = [(key_of[_key(lo)], key_of[_key(hi)], _key(fk)) for lo, hi, fk in want]
+            assert got_t == want_t, (R, pair)
+        skel = set(np.nonzero(skeleton_mask(mesh, dec))[0].tolist())
+        assert skel == {key_of[_key(c)] for c in case["skeleton"]}
+
+
+@pytest.mark.parametrize("name", ["uniform3", "uniform9", "refined"])
 def test_against_reference_mesh(name):
     G = GOLDEN[name]
     cells = [_key(c) for c in G["cells"]]
@@ -100,7 +124,14 @@ def _worker(rank, world, port, q):
         peer_plan = exchange_plan(mesh, dec, p)
         ok &= bool(np.array_equal(peer_plan.faces[rank], plan.faces[p]))
         ok &= bool(torch.equal(recv[p], _payload(peer_plan, rank)))
-    dt = global_dt(dist, 0.1 * (rank + 1))
+    dt = global_dt(dist, 0.1 * (rank + 1), cfl=0.5)
+    quiet = global_dt(dist, None if rank == 1 else 0.3)       # a rank without a positive speed
+    try:
+        global_dt(dist, None)
+        none_raises = False
+    except Exception as e:  # EnclaveDgError on every rank
+        none_raises = type(e).__name__ == "EnclaveDgError"
+    ok &= quiet == 0.3 and none_raises
     q.put((rank, ok, len(plan.peers), float(dt)))
     dist.destroy_process_group()
 
@@ -118,7 +149,7 @@ def test_exchange_gloo_world2():
     res = sorted(q.get() for _ in range(2))
     assert [r[1] for r in res] == [True, True]
     assert [r[2] for r in res] == [1, 1]
-    assert [r[3] for r in res] == [0.1, 0.1]
+    assert [r[3] for r in res] == [0.5 * 0.1, 0.5 * 0.1]
 
 
 @pytest.mark.gpu

@@ -7,7 +7,7 @@ neighbour-table entry point (`edg_corrector` with `nbr`) use the
 one-CTA-per-group kernel (`corrector_kernel<..., FUSED>`, edg_faces.cuh).  Both
 restate kernels.py:162-193 with the same operation order, so on the same
 predictor output they must give identical bits, including the next step's dt
-candidates.  The grids below are large enough for the pipelined kernel.
+candidate.  The grids below are large enough for the pipelined kernel.
 """
 import numpy as np
 import pytest
@@ -50,7 +50,9 @@ def test_pipelined_corrector_equals_one_cta_per_group(name, N):
                                         trace_q=s.trace_q, dt_slots=slots_b, hmin=s.hmin, status=status)
     torch.cuda.synchronize()
     assert torch.equal(out_a, out_b)
-    assert torch.equal(slots_a, slots_b)
+    # the CTAs spread their candidates over the 256 slots by block index, so
+    # only the minimum (what edg_dt_finalize reads) is comparable
+    assert int(slots_a.min()) == int(slots_b.min())
     assert int(status[0].item()) == 0
 
 
