@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(cf.CONFIGS))
     ap.add_argument("--no-secondary", action="store_true", help="skip the cfg2 (configs[1]) secondary line item")
+    ap.add_argument("--lib", default=None, help="load this build of libenclavedg_b200.so (A/B of build_lib --variant)")
     ap.add_argument("--cfl", type=float, default=None, help="override the config's CFL safety")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -684,6 +685,9 @@ def measure_e2e(solver, Q0, dof, steps, ws, dist, dev):
 
 def main():
     args = parse()
+    if args.lib:
+        from paper_1806_07984_b200 import _lib
+        _lib.load(args.lib)
     cfg = cf.CONFIGS[args.config]
     if args.cfl is not None:
         cfg = cfg.with_(cfl=args.cfl)

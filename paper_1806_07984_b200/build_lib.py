@@ -46,7 +46,7 @@ def _compile(src, obj, defines=()):
 
 def build(jobs=None, force=False, verbose=True, defines=(), variant=None):
     """Build the library; `defines` (e.g. EDG_FV_CPT=1) with a `variant` name
-    go to _lib/<variant>/ for A/B experiments (load with EDG_LIB=<path>)."""
+    go to _lib/<variant>/ for A/B experiments (bench.py --lib <path>)."""
     out_dir = OUT_DIR if variant is None else os.path.join(OUT_DIR, variant)
     lib = os.path.join(out_dir, "libenclavedg_b200.so")
     os.makedirs(out_dir, exist_ok=True)

@@ -1,0 +1,351 @@
+// 3-D space-time predictor (Picard), pencil formulation -- replaces
+// kernels.py:120-159 for 3-D cells of n >= 5 nodes per axis (one cell per CTA).
+//
+// The per-node kernel of edg_stp.cuh contracts every spatial derivative in
+// the thread of the node it belongs to: 3 axes x n loads of the flux per
+// component and time node, which made it shared-memory bound (ncu on cfg3:
+// the derivative loads were 38 % of the instructions and ~48 % of the stall
+// samples, 2.3 wavefronts per LDS.64).  Here one iteration of a cell runs in
+// three phases per group of G time nodes:
+//
+//   A  node threads: flux F_a(qhat_s) of their node for s in the group,
+//      stored into the rows [a][s][k] of the flux buffer, each axis in its own
+//      pencil-contiguous layout (node (i0,i1,i2) at n * pencil_a + i_a);
+//   B  pencil tasks (axis a, time node s, component k, pencil p): load the n
+//      flux values of the pencil, contract them with D (a constant-bank
+//      operand, so no register or shared load per FMA) and write
+//      (D F)/h_a back in place -- each flux value is read by exactly one task;
+//   C  node threads: dv = (H_0 + H_1) + H_2 at their node and the time
+//      contraction acc[r] += K^-1[r][s] (-dt w_s) dv.
+//
+// Shared-memory traffic per full iteration and cell drops from
+// 3 n^(d+1) m loads + d n^(d+1) m stores to 2 (d n^(d+1) m) loads + stores
+// (cfg3: 56k -> 37.5k accesses), and every pencil access is a stride-n lane
+// pattern that the row stride n^3 (= 13 mod 16 for n = 5) keeps at the ideal
+// two wavefronts per warp.  The Picard exit test, the exact reduced first
+// iteration, the persistent CTAs with cp.async prefetch and the epilogue are
+// those of edg_stp.cuh.
+#pragma once
+#include "edg_stp.cuh"
+
+namespace edg {
+
+// time nodes per phase group (all five at n = 5: 85 KB of shared memory and
+// 2 CTAs per SM; three for larger n so the rows stay under ~80 KB)
+#ifndef EDG_STP3_G
+#define EDG_STP3_G(n) ((n) <= 5 ? (n) : 3)
+#endif
+// resident CTAs per SM asked of ptxas (n = 5: 248 registers, no spills)
+#ifndef EDG_STP3_MINB
+#define EDG_STP3_MINB(n) ((n) <= 5 ? 2 : 1)
+#endif
+
+template <int KIND, int N>
+struct Stp3Cfg {
+  static constexpr int M = Pde<KIND, 3>::M;
+  static constexpr int NPC = N * N * N;
+  static constexpr int NF = N * N;
+  static constexpr int THREADS = ((NPC + 31) / 32) * 32;
+  static constexpr int G = EDG_STP3_G(N) < N ? EDG_STP3_G(N) : N;   // time nodes per group
+  static constexpr int ROW = NPC;                             // one (axis, time node, component) row
+  static constexpr int FBUF = 3 * G * M * ROW;
+  static constexpr int STAGE = (1 + 3) * M * NPC;             // epilogue staging [(1+d) M][NPC]
+  static constexpr int SF = FBUF > STAGE ? FBUF : STAGE;
+  static constexpr int OPS = 2 * N + 2;                        // c = K^-1 lift, sum_s B[r][s]
+  static constexpr size_t BYTES = sizeof(double) * (OPS + SF + 2 * M * NPC);
+  static constexpr int MINB = EDG_STP3_MINB(N);
+};
+
+template <int KIND, int N>
+__global__ void __launch_bounds__(Stp3Cfg<KIND, N>::THREADS, Stp3Cfg<KIND, N>::MINB)
+stp_picard3_kernel(const StpArgs A) {
+  const TraceScope trace_scope(A.trace);
+  using Cf = Stp3Cfg<KIND, N>;
+  constexpr int DIM = 3;
+  constexpr int M = Cf::M, NPC = Cf::NPC, NF = Cf::NF, THREADS = Cf::THREADS, G = Cf::G, ROW = Cf::ROW;
+  constexpr int O = pen_off(N);   // this order's block in the constant-bank operator table
+
+  extern __shared__ __align__(16) double smem[];
+  double* sC = smem;                 // K^-1 lift
+  double* sBs = sC + N;              // sum_s B[r][s]
+  double* sF = smem + Cf::OPS;       // flux / derivative rows [a][g][k][ROW]
+  double* sQ0 = sF + Cf::SF;         // initial state [2][M][NPC] (thread-private)
+  __shared__ double sIh[DIM];
+
+  const int tid = threadIdx.x;
+  const int node = tid;
+  const bool lane_ok = node < NPC;
+  const int nd = lane_ok ? node : 0;   // idle lanes read (and never write) node 0's rows
+  const int i0 = nd / NF, i1 = (nd / N) % N, i2 = nd % N;
+  // position of this node in axis a's pencil-contiguous layout
+  const int pos[DIM] = {N * (i1 * N + i2) + i0, N * (i0 * N + i2) + i1, N * (i0 * N + i1) + i2};
+  const double dt = *A.dt;
+  const int nblocks = A.nwork;
+
+  auto prefetch_q = [&](int b, int buf) {
+    if (lane_ok && b < A.nwork) {
+      const int c = A.cell_list ? __ldg(A.cell_list + b) : b;
+      const double* src = A.q + (size_t)c * M * NPC + node;
+      double* dst = sQ0 + buf * M * NPC + node;
+#pragma unroll
+      for (int k = 0; k < M; ++k) cp_async8(dst + k * NPC, src + k * NPC);
+    }
+  };
+  int blk = blockIdx.x;
+  if (blk < nblocks) prefetch_q(blk, 0);
+  cp_async_commit();
+  for (int i = tid; i < N; i += THREADS) {
+    sC[i] = A.basis[EDG_BASIS_KLIFT(N) + i];
+    double bs = 0.0;
+    for (int s = 0; s < N; ++s) bs += A.basis[EDG_BASIS_KINV(N) + i * N + s] * (-dt * A.basis[EDG_BASIS_W(N) + s]);
+    sBs[i] = bs;
+  }
+  if (!A.edges_per_cell && tid < DIM) sIh[tid] = 1.0 / A.edges[tid];
+  unsigned its_sum = 0u;
+
+  for (int gi = 0; blk < nblocks; blk += gridDim.x, ++gi) {
+    const int cell = A.cell_list ? __ldg(A.cell_list + blk) : blk;
+    if (blk + (int)gridDim.x < nblocks) prefetch_q(blk + gridDim.x, (gi + 1) & 1);
+    cp_async_commit();
+    if (A.edges_per_cell && tid < DIM) sIh[tid] = 1.0 / A.edges[(size_t)cell * DIM + tid];
+    cp_async_wait1();
+    __syncthreads();   // operators, 1/h, flags (and the previous block's epilogue reads) settled
+
+    const double* const q0s = sQ0 + (gi & 1) * M * NPC + node;
+    double qh[N][M], acc[N][M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double v = lane_ok ? q0s[k * NPC] : 1.0;
+#pragma unroll
+      for (int r = 0; r < N; ++r) qh[r][k] = v;
+    }
+
+    // ---- phase helpers -------------------------------------------------
+    // A: flux of time node s (group slot g) at this node -> rows [a][g][k]
+    auto put_flux = [&](int g, const double* q) {
+      double F[DIM][M];
+      FastFlux<KIND, DIM>::template all<M>(q, A.pp, F);
+      if (lane_ok) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+#pragma unroll
+          for (int k = 0; k < M; ++k) sF[((a * G + g) * M + k) * ROW + pos[a]] = F[a][k];
+      }
+    };
+    // B: in-place pencil contraction of the rows of group slots [0, ng)
+    auto pencils = [&](int ng) {
+      const int tasks = DIM * ng * M * NF;
+      for (int t = tid; t < tasks; t += THREADS) {
+        const int rg = t / NF, p = t - rg * NF;          // rg = (a, g, k) within the used slots
+        const int a = rg / (ng * M), rem = rg - a * ng * M;
+        double* P = sF + ((a * G) * M + rem) * ROW + p * N;
+        double f[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) f[j] = P[j];
+        const double ih = sIh[a];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double h = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) h = fma(kPen[O + EDG_BASIS_D(N) + i * N + j], f[j], h);
+          P[i] = h * ih;
+        }
+      }
+    };
+    // C: divergence of group slot g at this node
+    auto div_at = [&](int g, double (&dv)[M]) {
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        dv[k] = (sF[((0 * G + g) * M + k) * ROW + pos[0]] + sF[((1 * G + g) * M + k) * ROW + pos[1]]) +
+                sF[((2 * G + g) * M + k) * ROW + pos[2]];
+    };
+
+    int its = 0;
+    bool conv = false, inacc = false;
+    const int max_iter = A.max_iter;
+    // iteration exit (kernels.py:143-147): delta = max |new - qhat| < tol,
+    // NaN never below -- "every |new - qhat| < tol" per thread, OR-reduced
+    auto finish = [&](int it, bool below) -> bool {
+      const bool any = __syncthreads_or(lane_ok && !below);
+      its = it;
+      if (!any) conv = true;
+      return any;
+    };
+    bool any = false;
+    if (max_iter >= 1) {
+      // reduced first iteration: qhat_s = q for every s (kernels.py:134), so
+      //   acc[r] = c_r q + (sum_s B[r][s]) div F(q)
+      {
+        double q[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) q[k] = qh[0][k];
+        put_flux(0, q);
+      }
+      __syncthreads();
+      pencils(1);
+      __syncthreads();
+      double dv[M];
+      div_at(0, dv);
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+#pragma unroll
+        for (int r = 0; r < N; ++r) acc[r][k] = fma(sBs[r], dv[k], sC[r] * qh[r][k]);
+      bool below = true;
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int k = 0; k < M; ++k) below = below & (fabs(acc[r][k] - qh[r][k]) < A.tol);
+      inacc = true;
+      any = finish(1, below);
+    }
+    // full iteration: qn = c q + sum_s B[r][s] div F(qc_s); returns "not converged"
+    auto body = [&](const double (&qc)[N][M], double (&qn)[N][M], int it) -> bool {
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const double q0 = lane_ok ? q0s[k * NPC] : 1.0;
+#pragma unroll
+        for (int r = 0; r < N; ++r) qn[r][k] = kPen[O + EDG_BASIS_KLIFT(N) + r] * q0;
+      }
+#pragma unroll
+      for (int s0 = 0; s0 < N; s0 += G) {
+        const int ng = (N - s0) < G ? (N - s0) : G;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (g < ng) {
+            double q[M];
+#pragma unroll
+            for (int k = 0; k < M; ++k) q[k] = qc[s0 + g][k];
+            put_flux(g, q);
+          }
+        __syncthreads();
+        pencils(ng);
+        __syncthreads();
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (g < ng) {
+            double dv[M];
+            div_at(g, dv);
+            const double sc = -(dt * kPen[O + EDG_BASIS_W(N) + s0 + g]);   // (-dt) w_s
+#pragma unroll
+            for (int r = 0; r < N; ++r) {
+              const double b = kPen[O + EDG_BASIS_KINV(N) + r * N + s0 + g] * sc;
+#pragma unroll
+              for (int k = 0; k < M; ++k) qn[r][k] = fma(b, dv[k], qn[r][k]);
+            }
+          }
+        if (s0 + G < N) __syncthreads();   // the next group's fluxes overwrite the rows
+      }
+      bool below = true;
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int k = 0; k < M; ++k) below = below & (fabs(qn[r][k] - qc[r][k]) < A.tol);
+      return finish(it, below);   // the barrier also guards the rows for the next iteration
+    };
+    for (int it = 2; any && it <= max_iter;) {
+      any = body(acc, qh, it);
+      inacc = false;
+      if (!any || ++it > max_iter) break;
+      any = body(qh, acc, it);
+      inacc = true;
+      ++it;
+    }
+    if (inacc) {
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int k = 0; k < M; ++k) qh[r][k] = acc[r][k];
+    }
+
+    // ---------------------------------------------------------- epilogue --
+    // q_end = sum_r l_r(1) qhat_r; q_int = dt sum_r w_r qhat_r;
+    // fint_a = dt sum_r w_r F_a(qhat_r)     (kernels.py:148-155)
+    double* St = sF;
+    double qe[M], qi[M], fi[DIM][M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) qe[k] = qi[k] = 0.0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int k = 0; k < M; ++k) fi[a][k] = 0.0;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      const double tr = kPen[O + EDG_BASIS_TR(N) + r], w = kPen[O + EDG_BASIS_W(N) + r];
+      double F[DIM][M];
+      FastFlux<KIND, DIM>::template all<M>(qh[r], A.pp, F);
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        qe[k] = fma(tr, qh[r][k], qe[k]);
+        qi[k] = fma(w, qh[r][k], qi[k]);
+      }
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int k = 0; k < M; ++k) fi[a][k] = fma(w, F[a][k], fi[a][k]);
+    }
+    if (lane_ok) {
+      double* qend = A.q_end + (size_t)cell * M * NPC + node;
+      double* qint = A.q_int ? A.q_int + (size_t)cell * M * NPC + node : nullptr;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        qi[k] *= dt;
+        qend[k * NPC] = qe[k];
+        if (qint) qint[k * NPC] = qi[k];
+      }
+      if (node == 0) {
+        A.iterations[cell] = its;
+        A.converged[cell] = conv ? 1 : 0;
+        its_sum += (unsigned)its;
+      }
+#pragma unroll
+      for (int k = 0; k < M; ++k) St[k * NPC + node] = qi[k];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int k = 0; k < M; ++k) St[((1 + a) * M + k) * NPC + node] = fi[a][k] * dt;
+    }
+    __syncthreads();
+    // face projections, one task per (axis a, face point f): both sides of
+    // trace_q and trace_f for every component (kernels.py:73-79, 148-157)
+    for (int task = tid; task < DIM * NF; task += THREADS) {
+      constexpr int PER_FAM = 2 * DIM * M * NF;
+      const size_t tbase = (size_t)cell * PER_FAM;
+      const int a = task / NF, f = task - a * NF;
+      const int st = a == DIM - 1 ? 1 : (a == 0 ? NF : N);
+      const int hi = f / st, lo = f - hi * st;
+      const int base = hi * st * N + lo;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const double* sq = St + k * NPC + base;
+        const double* sf = St + ((1 + a) * M + k) * NPC + base;
+        double q0 = 0.0, q1 = 0.0, f0 = 0.0, f1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double vq = sq[j * st], vf = sf[j * st];
+          q0 = fma(kPen[O + EDG_BASIS_TL(N) + j], vq, q0);
+          q1 = fma(kPen[O + EDG_BASIS_TR(N) + j], vq, q1);
+          f0 = fma(kPen[O + EDG_BASIS_TL(N) + j], vf, f0);
+          f1 = fma(kPen[O + EDG_BASIS_TR(N) + j], vf, f1);
+        }
+        const size_t o0 = tbase + ((size_t)(2 * a) * M + k) * NF + f;
+        const size_t o1 = tbase + ((size_t)(2 * a + 1) * M + k) * NF + f;
+        A.trace_q[o0] = q0;
+        A.trace_q[o1] = q1;
+        A.trace_f[o0] = f0;
+        A.trace_f[o1] = f1;
+      }
+    }
+    // (the next block's first barrier orders these staging reads before its
+    // flux writes)
+  }  // work blocks
+  if (A.iter_total) {
+    __shared__ unsigned int sIts;
+    if (tid == 0) sIts = 0u;
+    __syncthreads();
+    if (its_sum) atomicAdd(&sIts, its_sum);
+    __syncthreads();
+    if (tid == 0 && sIts) atomicAdd(A.iter_total, (unsigned long long)sIts);
+  }
+}
+
+}  // namespace edg

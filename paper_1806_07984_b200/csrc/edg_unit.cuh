@@ -5,6 +5,7 @@
 #include <mutex>
 
 #include "edg_stp.cuh"
+#include "edg_stp3.cuh"
 #include "edg_stp_ck.cuh"
 #include "edg_faces.cuh"
 #include "edg_corr_pipe.cuh"
@@ -81,9 +82,33 @@ static int upload_ops(const double* basis, cudaStream_t st) {
   return EDG_OK;
 }
 
+#ifndef EDG_STP3
+#define EDG_STP3 1
+#endif
 template <int N>
 static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  if constexpr (DIM == 3 && N >= 5 && EDG_STP3) {
+    // 3-D, one cell per CTA: the pencil formulation (edg_stp3.cuh)
+    using C3 = Stp3Cfg<KIND, N>;
+    auto kern = stp_picard3_kernel<KIND, N>;
+    if (set_smem(kern, C3::BYTES)) return EDG_ERR_CUDA;
+    if (upload_ops<N>(a.basis, st)) return EDG_ERR_CUDA;
+    const int blocks = a.nwork;
+    int cap = persistent_grid(kern, C3::THREADS, C3::BYTES);
+    if (cap < 0) return EDG_ERR_CUDA;
+    if (a.ctas_per_sm < 0) {
+      cap = blocks;
+    } else if (a.ctas_per_sm > 0) {
+      int dev = 0, sms = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return EDG_ERR_CUDA;
+      if (sms * a.ctas_per_sm < cap) cap = sms * a.ctas_per_sm;
+    }
+    const int grid = blocks < cap ? blocks : cap;
+    if (grid > 0) kern<<<grid, C3::THREADS, C3::BYTES, st>>>(a);
+    return check_launch();
+  }
   using Cf = StpCfg<DIM, N>;
   const size_t smem = StpSmem<KIND, DIM, N>::BYTES;
   auto kern = stp_picard_kernel<KIND, DIM, N>;

@@ -103,9 +103,9 @@ def face_transfer_batch(order: int, traces, child_pos, restrict_mode: bool):
 # --------------------------------------------------------------------------
 # Cell-local operators of dynamic AMR:
 # transfer.py:99-158 of the reference on the sm_100a kernels of
-# csrc/edg_amr.cuh.  Mesh mutation itself (plan_mesh_updates /
-# apply_mesh_updates, transfer.py:161-219) stays host-side topology work and
-# is not part of this package.
+# csrc/edg_amr.cuh.  The mesh mutation (plan_mesh_updates /
+# apply_mesh_updates, transfer.py:161-219) is host-side topology work and
+# lives in amr.py, which calls these operators to migrate the state.
 
 def _vol_dev(x):
     x, host = _dev(x)
