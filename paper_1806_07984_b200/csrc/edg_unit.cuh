@@ -19,7 +19,7 @@
 #if EDG_UNIT_DIM == 2
 #define EDG_FOR_N(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
 #else
-#define EDG_FOR_N(X) X(2) X(3) X(4) X(5) X(6)
+#define EDG_FOR_N(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
 #endif
 
 namespace edg {
@@ -85,41 +85,12 @@ static int upload_ops(const double* basis, cudaStream_t st) {
 #ifndef EDG_STP3
 #define EDG_STP3 1
 #endif
-template <int N>
-static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
-  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
-  if constexpr (DIM == 3 && N >= 5 && EDG_STP3) {
-    // 3-D, one cell per CTA: the pencil formulation (edg_stp3.cuh)
-    using C3 = Stp3Cfg<KIND, N>;
-    auto kern = stp_picard3_kernel<KIND, N>;
-    if (set_smem(kern, C3::BYTES)) return EDG_ERR_CUDA;
-    if (upload_ops<N>(a.basis, st)) return EDG_ERR_CUDA;
-    const int blocks = a.nwork;
-    int cap = persistent_grid(kern, C3::THREADS, C3::BYTES);
-    if (cap < 0) return EDG_ERR_CUDA;
-    if (a.ctas_per_sm < 0) {
-      cap = blocks;
-    } else if (a.ctas_per_sm > 0) {
-      int dev = 0, sms = 0;
-      if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-        return EDG_ERR_CUDA;
-      if (sms * a.ctas_per_sm < cap) cap = sms * a.ctas_per_sm;
-    }
-    const int grid = blocks < cap ? blocks : cap;
-    if (grid > 0) kern<<<grid, C3::THREADS, C3::BYTES, st>>>(a);
-    return check_launch();
-  }
-  using Cf = StpCfg<DIM, N>;
-  const size_t smem = StpSmem<KIND, DIM, N>::BYTES;
-  auto kern = stp_picard_kernel<KIND, DIM, N>;
+// persistent-CTA launch of a predictor kernel over `blocks` work blocks with
+// the launch's grid policy (StpArgs::ctas_per_sm)
+template <typename K>
+static int launch_stp_grid(K kern, int threads, size_t smem, int blocks, const StpArgs& a, cudaStream_t st) {
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
-  if (StpSmem<KIND, DIM, N>::KC) {
-    if (upload_ops<N>(a.basis, st)) return EDG_ERR_CUDA;
-  }
-  const int blocks = (a.nwork + Cf::CPB - 1) / Cf::CPB;
-  // persistent CTAs (the kernel strides over work blocks), capped per SM or
-  // one block per CTA as the launch's grid policy asks
-  int cap = persistent_grid(kern, Cf::THREADS, smem);
+  int cap = persistent_grid(kern, threads, smem);
   if (cap < 0) return EDG_ERR_CUDA;
   if (a.ctas_per_sm < 0) {
     cap = blocks;
@@ -130,8 +101,23 @@ static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
     if (sms * a.ctas_per_sm < cap) cap = sms * a.ctas_per_sm;
   }
   const int grid = blocks < cap ? blocks : cap;
-  if (grid > 0) kern<<<grid, Cf::THREADS, smem, st>>>(a);
+  if (grid > 0) kern<<<grid, threads, smem, st>>>(a);
   return check_launch();
+}
+
+template <int N>
+static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
+  constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
+  if (upload_ops<N>(a.basis, st)) return EDG_ERR_CUDA;   // constant-bank operators of order N
+  if constexpr (DIM == 3 && N >= 5 && EDG_STP3) {
+    // 3-D, one cell per CTA: the pencil formulation (edg_stp3.cuh)
+    using C3 = Stp3Cfg<KIND, N>;
+    return launch_stp_grid(stp_picard3_kernel<KIND, N>, C3::THREADS, C3::BYTES, a.nwork, a, st);
+  } else {
+    using Cf = StpCfg<DIM, N>;
+    return launch_stp_grid(stp_picard_kernel<KIND, DIM, N>, Cf::THREADS, StpSmem<KIND, DIM, N>::BYTES,
+                           (a.nwork + Cf::CPB - 1) / Cf::CPB, a, st);
+  }
 }
 
 template <int N>
@@ -281,7 +267,7 @@ int EDG_FN(_max_n)() {
 #if EDG_UNIT_DIM == 2
   return 8;
 #else
-  return 6;
+  return 8;
 #endif
 }
 

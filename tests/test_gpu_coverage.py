@@ -29,8 +29,8 @@ def _states(rng, name, dim, n, C):
     return (1.0 + 0.05 * rng.standard_normal(shape))[:, None]
 
 
-CASES = [(name, 2, p) for name in ("euler", "advection", "burgers") for p in range(1, 8)] + \
-        [(name, 3, p) for name in ("euler", "advection", "burgers") for p in range(1, 6)]
+# every order the reference accepts (basis.py:13-14: p in [1, 7]) in 2-D and 3-D
+CASES = [(name, dim, p) for dim in (2, 3) for name in ("euler", "advection", "burgers") for p in range(1, 8)]
 
 
 @pytest.mark.parametrize("name,dim,p", CASES)
@@ -54,6 +54,24 @@ def test_every_instantiation_matches_oracle(edg, name, dim, p):
     tf = out["trace_f"].cpu().numpy()
     for j, k in enumerate(keys):
         assert rel_linf(tf[:, j], ref["trace_f"][k]) < 1e-12
+
+
+@pytest.mark.parametrize("p", [6, 7])
+def test_3d_high_order_steps_vs_oracle(edg, p):
+    """3-D Euler at the paper's highest orders (Table 1 measures p = 7,
+    PAPER.md:1788-1793): two whole steps on a 3^3 outflow grid against the
+    oracle's Algorithm-1 driver."""
+    from oracle import drivers, ops
+    cfg = edg.configs.CONFIGS["cfg3"].with_(cells=3, order=p)
+    Q0 = edg.configs.initial_dg_uniform(cfg)
+    s = edg.solver.DGSolver(edg.pde.euler(3), p, edg.mesh.CartesianMesh(3, 3, False), cfg.cfl)
+    s.set_state(Q0)
+    s.run(2, graph=False)
+    s.check_status()
+    Qo, log = drivers.dg_uniform_run(Q0, ops.euler(3), p, 3, 3, False, cfg.cfl, 2)
+    assert rel_linf(s.state().cpu().numpy(), Qo) <= 1e-10
+    assert rel_linf(s.dt_history(), np.array(log["dt"])) <= 1e-13
+    assert np.array_equal(s.iterations.cpu().numpy(), log["iterations"][-1])
 
 
 def test_empty_batches(edg):

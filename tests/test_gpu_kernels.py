@@ -170,11 +170,14 @@ def test_project_to_faces_matches_oracle(edg):
 
 
 def test_unsupported_order_is_config_error(edg):
-    with pytest.raises(edg.errors.ConfigError):
-        edg.kernels.stp_picard(np.ones((5,) + (8,) * 3), edg.pde.euler(3), 1e-4, edg.basis.get_basis(7),
-                               (0.1, 0.1, 0.1))
-    with pytest.raises(edg.errors.ConfigError):
-        edg.basis.get_basis(8)
+    """Orders outside the reference's [1, 7] (basis.py:13-14) are a ConfigError,
+    on the host (basis) and at the C ABI (edg_supported)."""
+    for p in (0, 8):
+        with pytest.raises(edg.errors.ConfigError):
+            edg.basis.get_basis(p)
+        for dim in (2, 3):
+            with pytest.raises(edg.errors.ConfigError):
+                edg.kernels._check_supported(edg.pde.euler(dim), p)
 
 
 def test_grid_and_table_paths_agree_bitwise(edg):

@@ -33,7 +33,7 @@ def test_supported_matrix():
     e3 = pde.euler(3).native()
     e2 = pde.euler(2).native()
     assert lib.edg_supported(ctypes.byref(e2), 5) and lib.edg_supported(ctypes.byref(e2), 7)
-    assert lib.edg_supported(ctypes.byref(e3), 4) and not lib.edg_supported(ctypes.byref(e3), 6)
+    assert lib.edg_supported(ctypes.byref(e3), 4) and lib.edg_supported(ctypes.byref(e3), 7)
     bad = _lib.make_pde_struct("euler", 2, 5)
     assert not lib.edg_supported(ctypes.byref(bad), 3)
 
