@@ -151,13 +151,6 @@ __device__ __forceinline__ double fast_rcp(double x) {
 
 template <int KIND, int DIM>
 struct FastFlux {
-  // flux along axis a only
-  template <int M>
-  __device__ __forceinline__ static void axis(const double* q, const PdeParams& pp, int a, double (&F)[M]) {
-    using P = Pde<KIND, DIM>;
-    const auto pr = P::parts(q, pp);
-    P::flux(q, pr, a, pp, F);
-  }
   // all-axes flux F[a][k] of one state
   template <int M>
   __device__ __forceinline__ static void all(const double* q, const PdeParams& pp, double (&F)[DIM][M]) {
@@ -170,21 +163,6 @@ struct FastFlux {
 
 template <int DIM>
 struct FastFlux<EDG_PDE_EULER, DIM> {
-  // flux along axis a only (same operations as all())
-  template <int M>
-  __device__ __forceinline__ static void axis(const double* q, const PdeParams& pp, int a, double (&F)[M]) {
-    const double inv = fast_rcp(q[0]);
-    double ke = q[1] * q[1];
-#pragma unroll
-    for (int i = 1; i < DIM; ++i) ke = fma(q[1 + i], q[1 + i], ke);
-    const double p = pp.gm1 * fma(-0.5 * ke, inv, q[1 + DIM]);
-    const double ep = q[1 + DIM] + p;
-    const double u = q[1 + a] * inv;
-    F[0] = q[1 + a];
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) F[1 + i] = (i == a) ? fma(q[1 + i], u, p) : q[1 + i] * u;
-    F[1 + DIM] = ep * u;
-  }
   template <int M>
   __device__ __forceinline__ static void all(const double* q, const PdeParams& pp, double (&F)[DIM][M]) {
     const double inv = fast_rcp(q[0]);

@@ -65,24 +65,28 @@ struct FvCfg {
   static constexpr int MINB = THREADS <= 256 ? 3 : 2;
 };
 
+// EDG_FV_IFACE (default 1): every interface flux of the patch is evaluated
+// ONCE per CTA into shared memory (axis by axis), then the volumes apply
+// their two interfaces; otherwise every volume evaluates its six interfaces
+// itself (each interior interface twice, by both neighbours)
+#ifndef EDG_FV_IFACE
+#define EDG_FV_IFACE 1
+#endif
+
 template <int KIND, int DIM, int K>
 struct FvSmem {
   static constexpr int M = Pde<KIND, DIM>::M;
-  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? (FvCfg<DIM, K>::Z4 ? 2 : 3) : 0;
-  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + DIM) + sizeof(unsigned long long) * DIM;
-  // persistent grid kernel: + raw staging of the next patch (interior + 2d halo layers)
-  static constexpr int RAW = M * FvCfg<DIM, K>::NC + 2 * DIM * M * FvCfg<DIM, K>::NL;
-  static constexpr size_t PIPE_BYTES = ((BYTES + 15) / 16) * 16 + 16 + sizeof(double) * RAW;
+  static constexpr bool IFACE = EDG_FV_IFACE;
+  static constexpr int NIF = (K + 1) * FvCfg<DIM, K>::NL;            // interfaces per axis
+  // staged parts: 1/rho, p, c (the volume-owner variant recomputes p under Z4)
+  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? ((FvCfg<DIM, K>::Z4 && !IFACE) ? 2 : 3) : 0;
+  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + (IFACE ? M * NIF : 0) + DIM) +
+                                  sizeof(unsigned long long) * DIM;
 };
 
-// One patch b.  PIPE = false: states read from global memory (one CTA per
-// patch).  PIPE = true: states read from the raw staging block sRaw, which the
-// persistent kernel below fills with cp.async while the previous patch is
-// being updated; `after_stage` runs right after the staging barrier (the
-// persistent kernel issues the next patch's copies there).
-template <int KIND, int DIM, int K, bool PIPE, typename AfterStage>
-__device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, double* smem, const double* sRaw,
-                                              AfterStage after_stage) {
+// One patch b (one CTA per patch; states read from global memory).
+template <int KIND, int DIM, int K>
+__device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, double* smem) {
   using P = Pde<KIND, DIM>;
   using Cf = FvCfg<DIM, K>;
   constexpr int M = P::M;
@@ -92,12 +96,16 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   // ext strides: last axis 1, then KEZ, then KEZ*KE
   auto estride = [](int ax) { return ax == DIM - 1 ? 1 : (ax == DIM - 2 ? KEZ : KEZ * KE); };
 
+  using Sm = FvSmem<KIND, DIM, K>;
+  constexpr bool IFACE = Sm::IFACE;
+  constexpr bool PREC = Cf::Z4 && !IFACE;          // pressure recomputed from the staged state
   double* sQ = smem;                               // [M][NE]
   double* sInv = sQ + M * NE;                      // [NE] (Euler)
   constexpr bool Z4 = Cf::Z4 && CPT == 2;
-  double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler; not staged when Z4)
-  double* sC = sP + ((EULER && !Cf::Z4) ? NE : 0); // [NE] (Euler) sound speed
-  unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sC + (EULER ? NE : 0));
+  double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler; not staged when PREC)
+  double* sC = sP + ((EULER && !PREC) ? NE : 0);   // [NE] (Euler) sound speed
+  double* sIf = sC + (EULER ? NE : 0);             // IFACE: [M][NIF] interface fluxes of one axis
+  unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sIf + (IFACE ? M * Sm::NIF : 0));
   double* sCoef = reinterpret_cast<double*>(sLam + DIM);   // [DIM] dt / (edge / K)
 
   const int tid = threadIdx.x;
@@ -126,7 +134,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
     if constexpr (EULER) {
       const auto pr = P::parts(q, A.pp);
       sInv[x] = pr.inv;
-      if constexpr (!Cf::Z4) sP[x] = pr.p;
+      if constexpr (!PREC) sP[x] = pr.p;
       sC[x] = __dsqrt_rn(__dmul_rn(__dmul_rn(A.pp.gamma, pr.p), pr.inv));
     }
   };
@@ -136,7 +144,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
     if constexpr (EULER) {
       const double inv = sInv[x];
       double p;
-      if constexpr (Cf::Z4) {
+      if constexpr (PREC) {
         // parts() pressure from the staged state and 1/rho (same operations)
         double ke = __dmul_rn(s.q[1], s.q[1]);
 #pragma unroll
@@ -177,7 +185,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   for (int u = 0; u < NIT; ++u) {
     const int c = tid + u * THREADS;
 #pragma unroll
-    for (int k = 0; k < M; ++k) qi_[u][k] = c < NC ? (PIPE ? sRaw[k * NC + c] : __ldg(src + k * NC + c)) : 0.0;
+    for (int k = 0; k < M; ++k) qi_[u][k] = c < NC ? __ldg(src + k * NC + c) : 0.0;
   }
 #pragma unroll
   for (int u = 0; u < NHT; ++u) {
@@ -197,10 +205,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
 #pragma unroll
       for (int ax = 0; ax < DIM; ++ax) x += (ax == a ? (s ? K + 1 : 0) : e[ax] + 1) * estride(ax);
       xh_[u] = x;
-      if (PIPE) {
-#pragma unroll
-        for (int k = 0; k < M; ++k) qh_[u][k] = sRaw[M * NC + (fs * M + k) * NL + f];
-      } else if (A.halos) {
+      if (A.halos) {
 #pragma unroll
         for (int k = 0; k < M; ++k) qh_[u][k] = __ldg(A.halos + (((size_t)b * 2 * DIM + fs) * M + k) * NL + f);
       } else {
@@ -238,15 +243,74 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   // dt / dx_a, once per CTA (kernels.py:241: dt / (h / k) with exact divisions)
   if (tid < DIM) sCoef[tid] = __ddiv_rn(*A.dt, __ddiv_rn(A.edges[tid], (double)K));
   __syncthreads();
-  after_stage();
 
+  double o[CPT][M];
+  int cv[CPT];   // own volumes
+  if constexpr (IFACE) {
+    // ---- every interface once: per axis a, the (K+1) K^(d-1) interface
+    // fluxes into sIf (threads over interfaces, the last ext axis fastest),
+    // then each thread applies them to its own volumes tid + j * THREADS in
+    // the reference's axis order (kernels.py:240-252) ----
+    constexpr int NIF = Sm::NIF;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      cv[j] = tid + j * THREADS;
+      const int x = ext_of_cell(cv[j] < NC ? cv[j] : 0);
+#pragma unroll
+      for (int k = 0; k < M; ++k) o[j][k] = sQ[k * NE + x];
+    }
+#pragma unroll 1
+    for (int a = 0; a < DIM; ++a) {
+      const int st = estride(a);
+      for (int i = tid; i < NIF; i += THREADS) {
+        // interface coordinates, row-major with extent K+1 on axis a and K elsewhere;
+        // lower state at ext coordinate c_a on axis a, c_b + 1 elsewhere
+        int x = 0, t = i;
+#pragma unroll
+        for (int ax = DIM - 1; ax >= 0; --ax) {
+          const int ext = ax == a ? K + 1 : K;
+          const int c = t % ext;
+          t /= ext;
+          x += (ax == a ? c : c + 1) * estride(ax);
+        }
+        State lo, hi;
+        double f[M];
+        load(x, lo);
+        load(x + st, hi);
+        iface(lo, hi, a, f);
+#pragma unroll
+        for (int k = 0; k < M; ++k) sIf[k * NIF + i] = f[k];
+      }
+      __syncthreads();
+      const double coef = sCoef[a];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        if (cv[j] < NC) {
+          // lower interface of volume v along a: coordinates (v_a on a, v_b elsewhere)
+          int il = 0, sa = 1, mul = 1, t = cv[j];
+#pragma unroll
+          for (int ax = DIM - 1; ax >= 0; --ax) {
+            const int v = t % K;
+            t /= K;
+            if (ax == a) sa = mul;
+            il += v * mul;
+            mul *= ax == a ? K + 1 : K;
+          }
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            o[j][k] = __dsub_rn(o[j][k], __dmul_rn(coef, __dsub_rn(sIf[k * NIF + il + sa], sIf[k * NIF + il])));
+        }
+      }
+      __syncthreads();   // the next axis overwrites sIf
+    }
+  } else {
   // ---- own volumes (CPT consecutive along the last axis) ----
   // volumes c0 + j * DZ: consecutive pairs, or (Z4) z and z + k/2
   constexpr int DZ = Z4 ? K / 2 : 1;
   const int c0 = Z4 ? (tid / (K / 2)) * K + tid % (K / 2) : tid * CPT;
-  const bool ok = c0 < NC;
-  const int x0 = ok ? ext_of_cell(c0) : ext_of_cell(0);
-  double o[CPT][M];
+  const int x0 = c0 < NC ? ext_of_cell(c0) : ext_of_cell(0);
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) cv[j] = c0 + j * DZ;
   // EDG_FV_JOUTER=1 (with Z4): volume-outer loop order -- one volume's state,
   // both interface fluxes and its update are live at a time (the axis-outer
   // order keeps both volumes' states live: spills at the 3-CTA register cap)
@@ -316,6 +380,8 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   }
   }
 
+  }  // volume-owner variant
+
   // ---- write back, non-finite count, next-step dt candidate ----
   // The patch is the dt unit (admissible_dt with order 0 over its volumes):
   // per axis a NaN-propagating max over the volumes, then the python max over
@@ -326,8 +392,8 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   double lv[CPT][DIM];
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
-    const int c = c0 + j * DZ;
-    if (ok) {
+    const int c = cv[j];
+    if (c < NC) {
       bool finite = true;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
@@ -348,13 +414,13 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
     __syncthreads();
     const unsigned nb = *nanbits;
     double lmax = 0.0;
-    if (ok) {
 #pragma unroll
-      for (int j = 0; j < CPT; ++j)
+    for (int j = 0; j < CPT; ++j)
+      if (cv[j] < NC) {
 #pragma unroll
         for (int a = 0; a < DIM; ++a)
           if (!((nb >> a) & 1u)) lmax = lv[j][a] > lmax ? lv[j][a] : lmax;
-    }
+      }
     unsigned long long key = (unsigned long long)__double_as_longlong(lmax);   // >= 0, NaN-free
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -372,71 +438,11 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   }
 }
 
-template <int KIND, int DIM, int K, int MINB = FvCfg<DIM, K>::MINB>
+template <int KIND, int DIM, int K, int MINB = (FvSmem<KIND, DIM, K>::IFACE ? 2 : FvCfg<DIM, K>::MINB)>
 __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(const FvArgs A) {
   const TraceScope trace_scope(A.trace);
   extern __shared__ __align__(16) double smem[];
-  fv_patch_body<KIND, DIM, K, false>(A, blockIdx.x, smem, nullptr, [] {});
-}
-
-// Persistent patch-grid kernel (edg_fv_grid_step): CTAs walk patches
-// blockIdx.x, blockIdx.x + gridDim.x, ...; the next patch's interior (one
-// contiguous block, 16-byte cp.async) and its 2d halo layers (the neighbour
-// patches' boundary layers, or the own layer at an outflow side) are copied
-// into the raw staging block while the current patch is updated, so the
-// global-load latency is off the critical path.  Same arithmetic and bits as
-// fv_patch_kernel.
-template <int KIND, int DIM, int K>
-__global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, 2) fv_grid_pipe_kernel(const FvArgs A) {
-  using Cf = FvCfg<DIM, K>;
-  using Sm = FvSmem<KIND, DIM, K>;
-  constexpr int M = Pde<KIND, DIM>::M;
-  constexpr int NC = Cf::NC, NL = Cf::NL, THREADS = Cf::THREADS;
-  extern __shared__ __align__(16) double smem[];
-  double* const sRaw = smem + (Sm::BYTES + 7) / 8;   // after the patch block (16-byte aligned below)
-  double* const raw = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sRaw) + 15) & ~uintptr_t(15));
-  const int tid = threadIdx.x;
-  const int n = A.pgrid_n;
-  auto issue = [&](int b) {
-    // interior: contiguous [M][NC] block
-    cp_block<THREADS>(raw, A.patch + (size_t)b * M * NC, M * NC, tid);
-    // halos [2d][M][NL]
-    for (int e = tid; e < 2 * DIM * M * NL; e += THREADS) {
-      const int fs = e / (M * NL), r = e - fs * (M * NL);
-      const int k = r / NL, f = r - k * NL;
-      const int a = fs >> 1, s = fs & 1;
-      int ee[DIM], t = f;
-#pragma unroll
-      for (int ax = DIM - 1; ax >= 0; --ax) {
-        if (ax == a) continue;
-        ee[ax] = t % K;
-        t /= K;
-      }
-      int stride = 1;
-#pragma unroll
-      for (int ax = DIM - 1; ax > a; --ax) stride *= n;
-      const int ia = (b / stride) % n;
-      int j = ia + (s ? 1 : -1);
-      if (j < 0 || j >= n) j = A.periodic ? (j < 0 ? n - 1 : 0) : -1;
-      const int nb = j < 0 ? -1 : b + (j - ia) * stride;
-      ee[a] = nb >= 0 ? (s == 0 ? K - 1 : 0) : (s == 0 ? 0 : K - 1);
-      int c = 0;
-#pragma unroll
-      for (int ax = 0; ax < DIM; ++ax) c = c * K + ee[ax];
-      cp_async8(raw + M * NC + e, A.patch + (size_t)(nb >= 0 ? nb : b) * M * NC + (size_t)k * NC + c);
-    }
-    cp_async_commit();
-  };
-  int b = blockIdx.x;
-  if (b < A.npatches) issue(b);
-  for (; b < A.npatches; b += gridDim.x) {
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();   // this patch's raw block has landed; the previous patch is done with smem
-    const int nxt = b + gridDim.x;
-    fv_patch_body<KIND, DIM, K, true>(A, b, smem, raw, [&] {
-      if (nxt < A.npatches) issue(nxt);   // raw block consumed by the staging pass
-    });
-  }
+  fv_patch_body<KIND, DIM, K>(A, blockIdx.x, smem);
 }
 
 template <int DIM>

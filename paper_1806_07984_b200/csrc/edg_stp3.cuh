@@ -39,10 +39,6 @@ namespace edg {
 #ifndef EDG_STP3_MINB
 #define EDG_STP3_MINB(n) ((n) <= 5 ? 2 : 1)
 #endif
-// flux evaluated by the pencil tasks (n = 5; larger n spill at 255 registers)
-#ifndef EDG_STP3_FUSED
-#define EDG_STP3_FUSED(n) ((n) <= 5)
-#endif
 
 template <int KIND, int N>
 struct Stp3Cfg {
@@ -56,12 +52,7 @@ struct Stp3Cfg {
   static constexpr int STAGE = (1 + 3) * M * NPC;             // epilogue staging [(1+d) M][NPC]
   static constexpr int SF = FBUF > STAGE ? FBUF : STAGE;
   static constexpr int OPS = 2 * N + 2;                        // c = K^-1 lift, sum_s B[r][s]
-  // FUSED: the pencil tasks evaluate the flux themselves from the states of
-  // the group's time nodes (staged [g][k][node]); the derivative rows are in
-  // the natural node layout
-  static constexpr bool FUSED = EDG_STP3_FUSED(N);
-  static constexpr int QHB = FUSED ? G * M * NPC : 0;
-  static constexpr size_t BYTES = sizeof(double) * (OPS + SF + QHB + 2 * M * NPC);
+  static constexpr size_t BYTES = sizeof(double) * (OPS + SF + 2 * M * NPC);
   static constexpr int MINB = EDG_STP3_MINB(N);
 };
 
@@ -78,8 +69,7 @@ stp_picard3_kernel(const StpArgs A) {
   double* sC = smem;                 // K^-1 lift
   double* sBs = sC + N;              // sum_s B[r][s]
   double* sF = smem + Cf::OPS;       // flux / derivative rows [a][g][k][ROW]
-  double* sQH = sF + Cf::SF;         // FUSED: states of the group's time nodes [g][k][node]
-  double* sQ0 = sQH + Cf::QHB;       // initial state [2][M][NPC] (thread-private)
+  double* sQ0 = sF + Cf::SF;         // initial state [2][M][NPC] (thread-private)
   __shared__ double sIh[DIM];
 
   const int tid = threadIdx.x;
@@ -88,8 +78,7 @@ stp_picard3_kernel(const StpArgs A) {
   const int nd = lane_ok ? node : 0;   // idle lanes read (and never write) node 0's rows
   const int i0 = nd / NF, i1 = (nd / N) % N, i2 = nd % N;
   // position of this node in axis a's pencil-contiguous layout
-  const int pos[DIM] = {Cf::FUSED ? nd : N * (i1 * N + i2) + i0, Cf::FUSED ? nd : N * (i0 * N + i2) + i1,
-                        Cf::FUSED ? nd : N * (i0 * N + i1) + i2};
+  const int pos[DIM] = {N * (i1 * N + i2) + i0, N * (i0 * N + i2) + i1, N * (i0 * N + i1) + i2};
   const double dt = *A.dt;
   const int nblocks = A.nwork;
 
@@ -134,13 +123,6 @@ stp_picard3_kernel(const StpArgs A) {
     // ---- phase helpers -------------------------------------------------
     // A: flux of time node s (group slot g) at this node -> rows [a][g][k]
     auto put_flux = [&](int g, const double* q) {
-      if constexpr (Cf::FUSED) {
-        if (lane_ok) {
-#pragma unroll
-          for (int k = 0; k < M; ++k) sQH[(g * M + k) * NPC + node] = q[k];
-        }
-        return;
-      }
       double F[DIM][M];
       FastFlux<KIND, DIM>::template all<M>(q, A.pp, F);
       if (lane_ok) {
@@ -152,42 +134,6 @@ stp_picard3_kernel(const StpArgs A) {
     };
     // B: in-place pencil contraction of the rows of group slots [0, ng)
     auto pencils = [&](int ng) {
-      if constexpr (Cf::FUSED) {
-        // task (axis a, group slot g, pencil p): the n states of the pencil,
-        // their flux along a, and D (x) F_a for every component.  The axis is
-        // a compile-time loop; axis a's tasks start at thread 32 a (mod the
-        // CTA) so that the three axes of a small group run on different warps.
-        const int per_axis = ng * NF;
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-          const int stride = a == 0 ? NF : (a == 1 ? N : 1);
-          const double ih = sIh[a];
-          for (int t = (tid + THREADS - 32 * a) % THREADS; t < per_axis; t += THREADS) {
-            const int g = t / NF, p = t - g * NF;
-            const int base = a == 0 ? p : (a == 1 ? (p / N) * NF + p % N : p * N);
-            double F[N][M];
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-              double q[M];
-#pragma unroll
-              for (int k = 0; k < M; ++k) q[k] = sQH[(g * M + k) * NPC + base + j * stride];
-              FastFlux<KIND, DIM>::template axis<M>(q, A.pp, a, F[j]);
-            }
-#pragma unroll
-            for (int k = 0; k < M; ++k) {
-              double* P = sF + ((a * G + g) * M + k) * ROW + base;
-#pragma unroll
-              for (int i = 0; i < N; ++i) {
-                double h = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) h = fma(kPen[O + EDG_BASIS_D(N) + i * N + j], F[j][k], h);
-                P[i * stride] = h * ih;
-              }
-            }
-          }
-        }
-        return;
-      }
       const int tasks = DIM * ng * M * NF;
       for (int t = tid; t < tasks; t += THREADS) {
         const int rg = t / NF, p = t - rg * NF;          // rg = (a, g, k) within the used slots
