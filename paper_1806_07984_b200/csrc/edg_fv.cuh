@@ -65,22 +65,12 @@ struct FvCfg {
   static constexpr int MINB = THREADS <= 256 ? 3 : 2;
 };
 
-// EDG_FV_IFACE (default 1): every interface flux of the patch is evaluated
-// ONCE per CTA into shared memory (axis by axis), then the volumes apply
-// their two interfaces; otherwise every volume evaluates its six interfaces
-// itself (each interior interface twice, by both neighbours)
-#ifndef EDG_FV_IFACE
-#define EDG_FV_IFACE 1
-#endif
-
 template <int KIND, int DIM, int K>
 struct FvSmem {
   static constexpr int M = Pde<KIND, DIM>::M;
-  static constexpr bool IFACE = EDG_FV_IFACE;
-  static constexpr int NIF = (K + 1) * FvCfg<DIM, K>::NL;            // interfaces per axis
-  // staged parts: 1/rho, p, c (the volume-owner variant recomputes p under Z4)
-  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? ((FvCfg<DIM, K>::Z4 && !IFACE) ? 2 : 3) : 0;
-  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + (IFACE ? M * NIF : 0) + DIM) +
+  // staged parts: 1/rho, (p,) c -- under Z4 the pressure is recomputed
+  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? (FvCfg<DIM, K>::Z4 ? 2 : 3) : 0;
+  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + DIM) +
                                   sizeof(unsigned long long) * DIM;
 };
 
@@ -96,16 +86,13 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   // ext strides: last axis 1, then KEZ, then KEZ*KE
   auto estride = [](int ax) { return ax == DIM - 1 ? 1 : (ax == DIM - 2 ? KEZ : KEZ * KE); };
 
-  using Sm = FvSmem<KIND, DIM, K>;
-  constexpr bool IFACE = Sm::IFACE;
-  constexpr bool PREC = Cf::Z4 && !IFACE;          // pressure recomputed from the staged state
+  constexpr bool PREC = Cf::Z4;                    // pressure recomputed from the staged state
   double* sQ = smem;                               // [M][NE]
   double* sInv = sQ + M * NE;                      // [NE] (Euler)
   constexpr bool Z4 = Cf::Z4 && CPT == 2;
   double* sP = sInv + (EULER ? NE : 0);            // [NE] (Euler; not staged when PREC)
   double* sC = sP + ((EULER && !PREC) ? NE : 0);   // [NE] (Euler) sound speed
-  double* sIf = sC + (EULER ? NE : 0);             // IFACE: [M][NIF] interface fluxes of one axis
-  unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sIf + (IFACE ? M * Sm::NIF : 0));
+  unsigned long long* sLam = reinterpret_cast<unsigned long long*>(sC + (EULER ? NE : 0));
   double* sCoef = reinterpret_cast<double*>(sLam + DIM);   // [DIM] dt / (edge / K)
 
   const int tid = threadIdx.x;
@@ -246,64 +233,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
 
   double o[CPT][M];
   int cv[CPT];   // own volumes
-  if constexpr (IFACE) {
-    // ---- every interface once: per axis a, the (K+1) K^(d-1) interface
-    // fluxes into sIf (threads over interfaces, the last ext axis fastest),
-    // then each thread applies them to its own volumes tid + j * THREADS in
-    // the reference's axis order (kernels.py:240-252) ----
-    constexpr int NIF = Sm::NIF;
-#pragma unroll
-    for (int j = 0; j < CPT; ++j) {
-      cv[j] = tid + j * THREADS;
-      const int x = ext_of_cell(cv[j] < NC ? cv[j] : 0);
-#pragma unroll
-      for (int k = 0; k < M; ++k) o[j][k] = sQ[k * NE + x];
-    }
-#pragma unroll 1
-    for (int a = 0; a < DIM; ++a) {
-      const int st = estride(a);
-      for (int i = tid; i < NIF; i += THREADS) {
-        // interface coordinates, row-major with extent K+1 on axis a and K elsewhere;
-        // lower state at ext coordinate c_a on axis a, c_b + 1 elsewhere
-        int x = 0, t = i;
-#pragma unroll
-        for (int ax = DIM - 1; ax >= 0; --ax) {
-          const int ext = ax == a ? K + 1 : K;
-          const int c = t % ext;
-          t /= ext;
-          x += (ax == a ? c : c + 1) * estride(ax);
-        }
-        State lo, hi;
-        double f[M];
-        load(x, lo);
-        load(x + st, hi);
-        iface(lo, hi, a, f);
-#pragma unroll
-        for (int k = 0; k < M; ++k) sIf[k * NIF + i] = f[k];
-      }
-      __syncthreads();
-      const double coef = sCoef[a];
-#pragma unroll
-      for (int j = 0; j < CPT; ++j) {
-        if (cv[j] < NC) {
-          // lower interface of volume v along a: coordinates (v_a on a, v_b elsewhere)
-          int il = 0, sa = 1, mul = 1, t = cv[j];
-#pragma unroll
-          for (int ax = DIM - 1; ax >= 0; --ax) {
-            const int v = t % K;
-            t /= K;
-            if (ax == a) sa = mul;
-            il += v * mul;
-            mul *= ax == a ? K + 1 : K;
-          }
-#pragma unroll
-          for (int k = 0; k < M; ++k)
-            o[j][k] = __dsub_rn(o[j][k], __dmul_rn(coef, __dsub_rn(sIf[k * NIF + il + sa], sIf[k * NIF + il])));
-        }
-      }
-      __syncthreads();   // the next axis overwrites sIf
-    }
-  } else {
+  {
   // ---- own volumes (CPT consecutive along the last axis) ----
   // volumes c0 + j * DZ: consecutive pairs, or (Z4) z and z + k/2
   constexpr int DZ = Z4 ? K / 2 : 1;
@@ -438,7 +368,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   }
 }
 
-template <int KIND, int DIM, int K, int MINB = (FvSmem<KIND, DIM, K>::IFACE ? 2 : FvCfg<DIM, K>::MINB)>
+template <int KIND, int DIM, int K, int MINB = FvCfg<DIM, K>::MINB>
 __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(const FvArgs A) {
   const TraceScope trace_scope(A.trace);
   extern __shared__ __align__(16) double smem[];
