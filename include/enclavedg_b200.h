@@ -177,6 +177,15 @@ int edg_faces_rusanov(const edg_pde* pde, int32_t order, const double* basis_dev
                       const int32_t* axis_dev, const int32_t* cell_dev, const int8_t* kind_dev,
                       const int8_t* child_pos_dev, const double* trace_q_dev, double* outcomes_dev,
                       void* stream);
+/* Multi-level hanging-face chains (mesh.py:67-100, 355-424): as
+ * edg_faces_rusanov, with each leaf's virtual side interpolated from the
+ * coarse owner's trace along a chain of vdepth[f] levels; vpath is
+ * [F][max_depth][2] int8 transverse digits, coarsest level first
+ * (edg_faces_rusanov is the max_depth = 1 case). */
+int edg_faces_rusanov_chain(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t nfaces,
+                            const int32_t* axis_dev, const int32_t* cell_dev, const int8_t* kind_dev,
+                            const int8_t* vpath_dev, const int8_t* vdepth_dev, int32_t max_depth,
+                            const double* trace_q_dev, double* outcomes_dev, void* stream);
 int edg_faces_restrict(int32_t dim, int32_t m, int32_t order, const double* basis_dev,
                        int32_t nparents, const int32_t* parent_face_dev, const int32_t* children_dev,
                        const int8_t* child_pos_dev, double* outcomes_dev, void* stream);

@@ -125,6 +125,56 @@ def dg_uniform_step_percell(Q, pde, basis, N, dim, periodic, cfl, dt=None, cells
 
 # --------------------------------------------------------------- AMR DG ---
 
+def virtual_path(f):
+    """Digit tuples from the coarse owner's side face down to leaf face f
+    (outermost level last): a virtual side's trace is the owner's trace
+    interpolated one level at a time along this path (transfer.py:75-79
+    applied level by level -- the multi-level chains of mesh.py:67-100)."""
+    owner_level = min(f.owners[s][0] for s in (0, 1) if f.sides[s] == "virtual")
+    path, g = [], f
+    while g.level > owner_level:
+        path.append(g.child_pos)
+        g = g.parent
+    return path[::-1]
+
+
+def amr_face_outcomes(forest, stores, pde, ops_t, sweep):
+    """Leaf-face Rusanov outcomes and the parent outcomes restricted from
+    them (restrict_riemann, transfer.py:82-96), deepest parents first so that
+    a parent of a parent accumulates complete children.  With at most one
+    level between neighbours this is exactly the one-level scheme."""
+    outcome, acc = {}, {}
+    for f in forest.leaf_faces():
+        a = f.axis
+        side_tr = [None, None]
+        for s in (0, 1):
+            tag = f.sides[s]
+            if tag == "cell":
+                side_tr[s] = stores[f.owners[s]].trace_q[(a, 1 - s)]
+            elif tag == "virtual":
+                t = stores[f.owners[s]].trace_q[(a, 1 - s)]
+                for digits in virtual_path(f):
+                    t = to_virtual(ops_t, t, digits)
+                side_tr[s] = t
+        if f.sides[0] == "boundary":
+            side_tr[0] = side_tr[1]
+        if f.sides[1] == "boundary":
+            side_tr[1] = side_tr[0]
+        out = ops.rusanov(side_tr[0], side_tr[1], pde, a)
+        if f.parent is not None:
+            buf = acc.setdefault(f.parent.key, ParentAccumulator())
+            accumulate_restriction(ops_t, buf, out, f.child_pos, sweep)
+        outcome[f.key] = out
+    # parents, deepest level first; a parent with a parent restricts into it
+    for key in sorted(acc, key=lambda k: -k[1]):
+        outcome[key] = acc[key].outcome
+        par = forest.faces[key].parent
+        if par is not None:
+            buf = acc.setdefault(par.key, ParentAccumulator())
+            accumulate_restriction(ops_t, buf, outcome[key], forest.faces[key].child_pos, sweep)
+    return outcome
+
+
 def dg_amr_step(forest, Q, pde, basis, cfl, sweep=0, dt=None):
     """One Algorithm-1 step on a static adaptive mesh (per-cell kernels).
 
@@ -137,28 +187,7 @@ def dg_amr_step(forest, Q, pde, basis, cfl, sweep=0, dt=None):
                            pde, basis.order, cfl, dim)
     stores = {k: ops.predictor_picard(Q[k], pde, dt, basis, forest.cell_edges(k[0]))
               for k in forest.sfc}
-    outcome = {}
-    acc = {}
-    for f in forest.leaf_faces():
-        a = f.axis
-        side_tr = [None, None]
-        for s in (0, 1):
-            tag = f.sides[s]
-            if tag == "cell":
-                side_tr[s] = stores[f.owners[s]].trace_q[(a, 1 - s)]
-            elif tag == "virtual":
-                side_tr[s] = to_virtual(ops_t, stores[f.owners[s]].trace_q[(a, 1 - s)], f.child_pos)
-        if f.sides[0] == "boundary":
-            side_tr[0] = side_tr[1]
-        if f.sides[1] == "boundary":
-            side_tr[1] = side_tr[0]
-        out = ops.rusanov(side_tr[0], side_tr[1], pde, a)
-        if f.parent is not None:
-            buf = acc.setdefault(f.parent.key, ParentAccumulator())
-            accumulate_restriction(ops_t, buf, out, f.child_pos, sweep)
-        outcome[f.key] = out
-    for key, buf in acc.items():
-        outcome[key] = buf.outcome
+    outcome = amr_face_outcomes(forest, stores, pde, ops_t, sweep)
     Qn = {}
     for k in forest.sfc:
         res = {(a, s): outcome[forest.side_face_key(k, a, s)] for a in range(dim) for s in (0, 1)}

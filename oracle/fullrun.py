@@ -91,24 +91,7 @@ def amr_step(pool, cfg, forest, Q, sweep):
                        cfg.cfl, d)
     stl = pool.map(_stp_cell, [(Q[i], dt, forest.cell_edges(k[0])) for i, k in enumerate(keys)], chunksize=256)
     stores = dict(zip(keys, stl))
-    outcome, acc = {}, {}
-    for f in forest.leaf_faces():
-        a = f.axis
-        tr = [None, None]
-        for sd in (0, 1):
-            if f.sides[sd] == "cell":
-                tr[sd] = stores[f.owners[sd]].trace_q[(a, 1 - sd)]
-            elif f.sides[sd] == "virtual":
-                tr[sd] = transfer.to_virtual(ops_t, stores[f.owners[sd]].trace_q[(a, 1 - sd)], f.child_pos)
-        tr[0] = tr[1] if f.sides[0] == "boundary" else tr[0]
-        tr[1] = tr[0] if f.sides[1] == "boundary" else tr[1]
-        out = ops.rusanov(tr[0], tr[1], pde, a)
-        if f.parent is not None:
-            buf = acc.setdefault(f.parent.key, transfer.ParentAccumulator())
-            transfer.accumulate_restriction(ops_t, buf, out, f.child_pos, sweep)
-        outcome[f.key] = out
-    for key, buf in acc.items():
-        outcome[key] = buf.outcome
+    outcome = drivers.amr_face_outcomes(forest, stores, pde, ops_t, sweep)
     Qn = np.stack([ops.correct(stores[k], {(a, sd): outcome[forest.side_face_key(k, a, sd)]
                                             for a in range(d) for sd in (0, 1)}, basis, forest.cell_edges(k[0]))
                    for k in keys])

@@ -49,6 +49,7 @@ SIGNATURES = {
     "edg_dt_slots_reset": (C.c_int, [P, P]),
     "edg_dt_finalize": (C.c_int, [P, D, P, P, I32, P, P]),
     "edg_faces_rusanov": (C.c_int, [PDEP, I32, P, I32, P, P, P, P, P, P, P]),
+    "edg_faces_rusanov_chain": (C.c_int, [PDEP, I32, P, I32, P, P, P, P, P, I32, P, P, P]),
     "edg_faces_restrict": (C.c_int, [I32, I32, I32, P, I32, P, P, P, P, P]),
     "edg_interpolate_face_trace": (C.c_int, [I32, I32, I32, P, I32, P, P, I32, P, P]),
     "edg_fv_patch_update": (C.c_int, [PDEP, I32, I32, P, P, P, P, P, P]),

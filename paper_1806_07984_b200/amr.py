@@ -7,8 +7,8 @@ transfer.gradient_indicator_batch (edg_gradient_indicator), the volumetric
 data move with edg_interpolate_volume / edg_restrict_volume; only the
 topology bookkeeping (which cells split or merge) is host work, as in the
 reference.  Differences from the reference API: cells are addressed by their
-(level, index) keys instead of spacetree node objects, and the mesh supports
-at most one level between face neighbours (ConfigError otherwise).
+(level, index) keys instead of spacetree node objects, and hanging-face
+chains may span up to mesh.MAX_CHAIN levels (ConfigError beyond).
 """
 from __future__ import annotations
 
@@ -87,12 +87,14 @@ def apply_mesh_updates(mesh: AdaptiveMesh, verdicts: dict, solutions: dict, orde
     return delta, new_data
 
 
-def adapt(solver, decision: T.RefinementDecision, min_level: int = 0, **solver_kw):
+def adapt(solver, decision: T.RefinementDecision, min_level: int = 0, in_place: bool = True, **solver_kw):
     """One adaptation of a device-resident DGSolver on an AdaptiveMesh:
     indicator and verdicts of every cell on the GPU, the plan on the host,
     the new state assembled on the GPU (kept cells gathered, refined cells
-    interpolated, coarsened clusters restricted).  Returns (new solver on the
-    updated mesh with the migrated state, MeshDelta)."""
+    interpolated, coarsened clusters restricted).  With in_place (default)
+    the solver itself adopts the updated mesh (DGSolver.remesh: device tables
+    rebuilt, buffers reused while they fit); otherwise a new solver is built
+    and the old one keeps its mesh.  Returns (solver, MeshDelta)."""
     import copy
 
     from .solver import DGSolver
@@ -130,6 +132,9 @@ def adapt(solver, decision: T.RefinementDecision, min_level: int = 0, **solver_k
     if coarsen:
         dst = torch.tensor([mesh.pos[p] for p in coarsen], dtype=torch.long, device="cuda")
         newQ[dst] = par
+    if in_place:
+        solver.remesh(mesh, newQ)
+        return solver, delta
     kw = dict(tol=solver.tol, max_iter=solver.max_iter or None, check_finite=solver.check_finite,
               max_steps=solver.max_steps, two_streams=getattr(solver, "two_streams", True))
     kw.update(solver_kw)

@@ -298,25 +298,36 @@ int edg_dt_finalize(unsigned long long* dt_slots_dev, double cfl, double* dt_dev
   return cuda_status(check_launch());
 }
 
-int edg_faces_rusanov(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t nfaces,
-                      const int32_t* axis_dev, const int32_t* cell_dev, const int8_t* kind_dev,
-                      const int8_t* child_pos_dev, const double* trace_q_dev, double* outcomes_dev, void* stream) {
+int edg_faces_rusanov_chain(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t nfaces,
+                            const int32_t* axis_dev, const int32_t* cell_dev, const int8_t* kind_dev,
+                            const int8_t* vpath_dev, const int8_t* vdepth_dev, int32_t max_depth,
+                            const double* trace_q_dev, double* outcomes_dev, void* stream) {
   unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (order < 1 || order + 1 > u->max_n()) return fail(EDG_ERR_CONFIG, "polynomial order not built for this pde/dim");
+  if (max_depth < 1) return fail(EDG_ERR_CONFIG, "chain depth must be >= 1");
   FaceArgs a;
   a.basis = basis_dev;
   a.nfaces = nfaces;
   a.axis = axis_dev;
   a.cell = cell_dev;
   a.kind = kind_dev;
-  a.child_pos = child_pos_dev;
+  a.child_pos = vpath_dev;
+  a.vdepth = vdepth_dev;
+  a.maxd = max_depth;
   a.trace_q = trace_q_dev;
   a.outcomes = outcomes_dev;
   a.pp = params_of(pde);
   a.trace = trace;
   return cuda_status(u->faces(order + 1, a, (cudaStream_t)stream));
+}
+
+int edg_faces_rusanov(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t nfaces,
+                      const int32_t* axis_dev, const int32_t* cell_dev, const int8_t* kind_dev,
+                      const int8_t* child_pos_dev, const double* trace_q_dev, double* outcomes_dev, void* stream) {
+  return edg_faces_rusanov_chain(pde, order, basis_dev, nfaces, axis_dev, cell_dev, kind_dev, child_pos_dev, nullptr,
+                                 1, trace_q_dev, outcomes_dev, stream);
 }
 
 }  // extern "C"

@@ -272,7 +272,9 @@ struct FaceArgs {
   const int32_t* axis;
   const int32_t* cell;      // [F][2]
   const int8_t* kind;       // [F][2]
-  const int8_t* child_pos;  // [F][2]
+  const int8_t* child_pos;  // [F][maxd][2]: transverse digits per chain level, coarsest first
+  const int8_t* vdepth;     // [F] chain levels of the virtual side (null: 1)
+  int32_t maxd;
   const double* trace_q;
   double* outcomes;
   PdeParams pp;
@@ -280,11 +282,36 @@ struct FaceArgs {
 };
 
 // trace of one side at face point f: own trace, or the coarse owner's trace
-// evaluated at the child face's GL points (interpolate_to_virtual,
-// transfer.py:59-79; axes contracted in order like _apply_axes, transfer.py:51-56)
+// evaluated at the leaf face's GL points (interpolate_to_virtual,
+// transfer.py:59-79; axes contracted in order like _apply_axes,
+// transfer.py:51-56).  Across a chain of `depth` levels the owner's trace is
+// interpolated level by level (coarsest digit first), i.e. row f_t of
+// I[d_depth] ... I[d_1] along each transverse axis t; at depth 1 the rows are
+// those of I itself and the arithmetic is the one-level one.
+template <int N>
+__device__ __forceinline__ void chain_row(const double* interp, const int8_t* cp, int depth, int t, int ft,
+                                          double (&R)[N]) {
+  const double* I = interp + cp[2 * (depth - 1) + t] * N * N + ft * N;
+#pragma unroll
+  for (int l = 0; l < N; ++l) R[l] = I[l];
+  for (int j = depth - 2; j >= 0; --j) {
+    const double* J = interp + cp[2 * j + t] * N * N;
+    double r2[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) v = fma(R[m], J[m * N + l], v);
+      r2[l] = v;
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) R[l] = r2[l];
+  }
+}
+
 template <int DIM, int N, int M>
-__device__ __forceinline__ void side_state(const double* tr, int kind, const int8_t* cp, const double* interp,
-                                           int f, double* out) {
+__device__ __forceinline__ void side_state(const double* tr, int kind, const int8_t* cp, int depth,
+                                           const double* interp, int f, double* out) {
   constexpr int NF = ipow(N, DIM - 1);
   if (kind == 0) {
 #pragma unroll
@@ -292,18 +319,20 @@ __device__ __forceinline__ void side_state(const double* tr, int kind, const int
     return;
   }
   if (DIM == 2) {
-    const double* I = interp + cp[0] * N * N + f * N;
+    double R[N];
+    chain_row<N>(interp, cp, depth, 0, f, R);
 #pragma unroll
     for (int k = 0; k < M; ++k) {
       double v = 0.0;
 #pragma unroll
-      for (int l = 0; l < N; ++l) v = fma(I[l], tr[k * NF + l], v);
+      for (int l = 0; l < N; ++l) v = fma(R[l], tr[k * NF + l], v);
       out[k] = v;
     }
   } else {
     const int f1 = f / N, f2 = f % N;
-    const double* I1 = interp + cp[0] * N * N + f1 * N;
-    const double* I2 = interp + cp[1] * N * N + f2 * N;
+    double R1[N], R2[N];
+    chain_row<N>(interp, cp, depth, 0, f1, R1);
+    chain_row<N>(interp, cp, depth, 1, f2, R2);
 #pragma unroll
     for (int k = 0; k < M; ++k) {
       double v = 0.0;
@@ -311,8 +340,8 @@ __device__ __forceinline__ void side_state(const double* tr, int kind, const int
       for (int l2 = 0; l2 < N; ++l2) {
         double t = 0.0;
 #pragma unroll
-        for (int l1 = 0; l1 < N; ++l1) t = fma(I1[l1], tr[k * NF + l1 * N + l2], t);
-        v = fma(I2[l2], t, v);
+        for (int l1 = 0; l1 < N; ++l1) t = fma(R1[l1], tr[k * NF + l1 * N + l2], t);
+        v = fma(R2[l2], t, v);
       }
       out[k] = v;
     }
@@ -341,7 +370,8 @@ __global__ void __launch_bounds__(128) faces_rusanov_kernel(const FaceArgs A) {
       const int c = A.cell[2 * fc + s];
       // side s of the face is covered by the owner's face (a, 1 - s)
       const double* tr = A.trace_q + ((size_t)c * 2 * DIM + 2 * a + (1 - s)) * M * NF;
-      side_state<DIM, N, M>(tr, kinds[s], A.child_pos + 2 * fc, sI, f, st[s]);
+      side_state<DIM, N, M>(tr, kinds[s], A.child_pos + (size_t)fc * 2 * A.maxd, A.vdepth ? A.vdepth[fc] : 1, sI, f,
+                            st[s]);
     }
   }
   if (kinds[0] == 2)

@@ -5,15 +5,18 @@ Two mesh kinds cover the BASELINE configurations:
 * CartesianMesh -- uniform N^d cells, periodic or outflow, row-major cell
   order (configs 1-4; the reference's 3-partitioned tree only offers 3^k,
   SURVEY.md section 0).  Exports nbr[c][2a+s] (-1 = outflow).
-* AdaptiveMesh -- a static mesh of real cells (level, index) with at most one
-  level between face neighbours (config 5), in the reference's SFC order.
-  Builds the same face forest as the reference Mesh (mesh.py:346-483): a
-  coarse face whose other side is refined becomes a parent with 3^(d-1)
-  child faces in child_pos order, each child face having the fine cell on
-  one side and a virtual side (the coarse owner's trace interpolated,
-  transfer.py:75-79) on the other.  Exports the leaf-face list, the parent
-  list and side_face[c][2a+s] (an index into the outcome array: leaves
-  first, then parents), plus the skeleton / enclave split of the schedule.
+* AdaptiveMesh -- a mesh of real cells (level, index) in the reference's SFC
+  order (config 5), with up to MAX_CHAIN levels between face neighbours.
+  Builds the same face forest as the reference Mesh (mesh.py:67-100,
+  346-483): a coarse face whose other side is refined becomes a parent with
+  3^(d-1) child faces in child_pos order, recursively while the fine side is
+  refined further, and each leaf of such a chain has the fine cell on one
+  side and a virtual side on the other (the coarse owner's trace
+  interpolated level by level along the chain, transfer.py:75-79).  Exports
+  the leaf-face list (with each leaf's interpolation path), the parent list
+  (deepest level first, with per-level launch groups) and
+  side_face[c][2a+s] (an index into the outcome array: leaves first, then
+  parents), plus the skeleton / enclave split of the schedule.
 
 Skeleton rule (BASELINE.json config 5, pinned in DESIGN.md): a cell is
 skeleton iff one of its faces is hanging (coarse side of a parent face -- the
@@ -28,6 +31,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .errors import ConfigError
+
+MAX_CHAIN = 4      # levels a hanging-face chain may span (virtual-side interpolation path length)
 
 
 def _row_major_strides(N, dim):
@@ -122,8 +127,8 @@ class AdaptiveMesh:
         3^d clusters into their parents, then rebuild the face forest once
         (mesh.py:309-317).  Raises ConfigError for an invalid target (the
         reference's InvalidTargetError / NotCoarsenableError / CapacityError)
-        and for results with more than one level between face neighbours,
-        which this solver does not support.  Returns a MeshDelta."""
+        and for hanging-face chains longer than MAX_CHAIN levels.  Returns a
+        MeshDelta."""
         before_cells, before_faces = set(self.cells), self._face_keys()
         cells = set(self.cells)
         for key in refine_cells:
@@ -163,8 +168,9 @@ class AdaptiveMesh:
 
     def _build(self):
         d = self.dim
-        leaf = {}          # key -> dict(axis, cells[2], kinds[2], child_pos)
-        parents = {}       # key -> list of child keys
+        leaf = {}          # key -> dict(axis, cells[2], kinds[2], child_pos, vpath)
+        parents = {}       # key -> {digits: child key (leaf or parent)}
+        par_cp = {}        # parent key -> its digits within its own parent (None for a root)
         side_key = {}      # (cell, fs) -> face key (leaf or parent)
         for c in self.cells:
             level, idx = c
@@ -175,7 +181,7 @@ class AdaptiveMesh:
                     if not (0 <= j < n) and not self.periodic:
                         key = ("L", a, level, idx[:a] + (idx[a] + s,) + idx[a + 1:])
                         leaf[key] = dict(axis=a, cells=[self.pos[c], self.pos[c]],
-                                         kinds=[2, 0] if s == 0 else [0, 2], child_pos=(0, 0))
+                                         kinds=[2, 0] if s == 0 else [0, 2], child_pos=(0, 0), vpath=[])
                         side_key[(c, 2 * a + s)] = key
                         continue
                     nb = idx[:a] + (j % n,) + idx[a + 1:]
@@ -187,30 +193,40 @@ class AdaptiveMesh:
                     if cov is not None and cov[0] == level:
                         key = ("L", a, level, fpos)
                         lo, hi = (c, cov) if s == 1 else (cov, c)
-                        leaf[key] = dict(axis=a, cells=[self.pos[lo], self.pos[hi]], kinds=[0, 0], child_pos=(0, 0))
+                        leaf[key] = dict(axis=a, cells=[self.pos[lo], self.pos[hi]], kinds=[0, 0], child_pos=(0, 0),
+                                         vpath=[])
                         side_key[(c, 2 * a + s)] = key
                     elif cov is not None:
-                        if cov[0] != level - 1:
-                            raise ConfigError("AdaptiveMesh supports one level between face neighbours")
-                        # this fine cell sits on a child face of the coarse neighbour's face
-                        digits = tuple(idx[t] % 3 for t in range(d) if t != a)
-                        key = ("L", a, level, fpos)
+                        # this fine cell sits at the bottom of a chain of hanging faces
+                        # below the coarse neighbour's side face (mesh.py:67-100,
+                        # 378-420): parents at levels cov_level .. level-1, the leaf
+                        # at `level` with the coarse owner on its virtual side
+                        lc = cov[0]
+
+                        def digits_at(l):
+                            return tuple((idx[t] // 3 ** (level - l)) % 3 for t in range(d) if t != a)
+
+                        def key_at(l, kind):
+                            sh = 3 ** (level - l)
+                            return (kind, a, l, tuple(fpos[t] // sh for t in range(d)))
+
+                        vpath = [digits_at(l) for l in range(lc + 1, level + 1)]
+                        key = key_at(level, "L")
                         lo, hi = (c, cov) if s == 1 else (cov, c)
                         kinds = [0, 1] if s == 1 else [1, 0]
                         leaf[key] = dict(axis=a, cells=[self.pos[lo], self.pos[hi]], kinds=kinds,
-                                         child_pos=digits + (0,) * (2 - len(digits)))
+                                         child_pos=vpath[-1] + (0,) * (2 - len(vpath[-1])), vpath=vpath)
                         side_key[(c, 2 * a + s)] = key
-                        # parent face key of the coarse cell side (a, 1 - s)
-                        cl, ci = cov
-                        cn = 3 ** cl
-                        cup = ci[a] + (1 - s)
-                        if self.periodic and cup == cn:
-                            cup = 0
-                        pkey = ("P", a, cl, ci[:a] + (cup,) + ci[a + 1:])
-                        parents.setdefault(pkey, {})[digits] = key
+                        child = key
+                        for l in range(level - 1, lc - 1, -1):
+                            pk = key_at(l, "P")
+                            parents.setdefault(pk, {})[digits_at(l + 1)] = child
+                            par_cp.setdefault(pk, digits_at(l) if l > lc else None)
+                            child = pk
                     else:
                         key = ("P", a, level, fpos)
                         parents.setdefault(key, {})
+                        par_cp.setdefault(key, None)
                         side_key[(c, 2 * a + s)] = key
         # coarse cells' sides on parents
         nch = 3 ** (d - 1)
@@ -233,7 +249,9 @@ class AdaptiveMesh:
         leaf_keys = sorted(leaf, key=lambda k: (not on_skel[k], k[1], k[2], k[3]))
         self._leaf_keys = leaf_keys
         self.nleaf_skeleton = sum(on_skel.values())
-        par_keys = sorted(parents, key=lambda k: (k[1], k[2], k[3]))
+        # parents deepest level first (a parent is restricted after all of its
+        # children, which may be parents one level below), grouped by level
+        par_keys = sorted(parents, key=lambda k: (-k[2], k[1], k[3]))
         index = {k: i for i, k in enumerate(leaf_keys)}
         F = len(leaf_keys)
         for i, k in enumerate(par_keys):
@@ -243,11 +261,36 @@ class AdaptiveMesh:
         self.face_cell = np.array([leaf[k]["cells"] for k in leaf_keys], dtype=np.int32).reshape(F, 2)
         self.face_kind = np.array([leaf[k]["kinds"] for k in leaf_keys], dtype=np.int8).reshape(F, 2)
         self.face_child_pos = np.array([leaf[k]["child_pos"] for k in leaf_keys], dtype=np.int8).reshape(F, 2)
+        # virtual-side interpolation path of every leaf (coarsest level first)
+        depth = max([len(leaf[k]["vpath"]) for k in leaf_keys] + [1])
+        if depth > MAX_CHAIN:
+            raise ConfigError(f"hanging-face chains deeper than {MAX_CHAIN} levels are not supported")
+        self.max_chain = depth
+        self.face_vdepth = np.array([len(leaf[k]["vpath"]) for k in leaf_keys], dtype=np.int8)
+        self.face_vpath = np.zeros((F, MAX_CHAIN, 2), dtype=np.int8)
+        for i, k in enumerate(leaf_keys):
+            for l, dg in enumerate(leaf[k]["vpath"]):
+                self.face_vpath[i, l, :len(dg)] = dg
         digits_all = list(itertools.product(range(3), repeat=d - 1))
         self.parent_face = np.arange(F, F + self.nparent, dtype=np.int32)
         self.parent_children = np.array([[index[parents[k][dg]] for dg in digits_all] for k in par_keys],
                                         dtype=np.int32).reshape(self.nparent, nch)
-        if self.nparent and self.parent_children.max() >= self.nleaf_skeleton:
+        # child position of every outcome row within its parent (leaves and parents)
+        self.outcome_cp = np.zeros((F + self.nparent, 2), dtype=np.int8)
+        self.outcome_cp[:F] = self.face_child_pos
+        for i, k in enumerate(par_keys):
+            dg = par_cp.get(k)
+            if dg is not None:
+                self.outcome_cp[F + i, :len(dg)] = dg
+        # restriction launches: contiguous parent ranges of one level, deepest first
+        self.parent_groups = []
+        for i, k in enumerate(par_keys):
+            if self.parent_groups and par_keys[i - 1][2] == k[2]:
+                self.parent_groups[-1][1] += 1
+            else:
+                self.parent_groups.append([i, 1])
+        leaf_children = self.parent_children[self.parent_children < F]
+        if leaf_children.size and leaf_children.max() >= self.nleaf_skeleton:
             raise ConfigError("internal: a hanging child face is not on the skeleton")
         self.side_face = np.full((self.ncells, 2 * d), -1, dtype=np.int32)
         for (c, fs), k in side_key.items():

