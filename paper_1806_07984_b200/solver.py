@@ -374,7 +374,7 @@ class DGSolver(_Base):
         _lib.check(self.lib.edg_faces_rusanov_chain(C.byref(self.native), self.order, _lib.ptr(self.table), cnt,
                                                     _lib.ptr(self.face_axis[sl]), _lib.ptr(self.face_cell[sl]),
                                                     _lib.ptr(self.face_kind[sl]), _lib.ptr(self.face_vpath[sl]),
-                                                    _lib.ptr(self.face_vdepth[sl]), self.max_chain,
+                                                    _lib.ptr(self.face_vdepth[sl]), int(self.face_vpath.shape[1]),
                                                     _lib.ptr(self.trace_q), _lib.ptr(self.outcomes[sl]),
                                                     _stream()), "faces_rusanov")
 
