@@ -154,13 +154,24 @@ def skeleton_mask(mesh, decomp: DomainDecomposition | None):
 class ExchangePlan:
     """Per-rank view: for each neighbour rank, the shared faces (indices into
     interior_faces) and, per face, this rank's local owner cell and the
-    side (0 = lo, 1 = hi) that cell occupies."""
+    side (0 = lo, 1 = hi) that cell occupies.
+
+    Hanging faces (AdaptiveMesh): the payload of a face is always the local
+    owner's whole side trace (`local_fs`); when the local owner is the coarse
+    cell of a chain, the RECEIVER evaluates it at the leaf face's points with
+    the face's interpolation path (`vpath` / `vdepth`, coarsest level first,
+    the same path the device face kernel applies), exactly as it would for a
+    local coarse neighbour -- the reference sends the projection from the
+    local adjacent cell, which for the coarse owner is that
+    trace."""
     rank: int
     peers: list
     faces: dict          # peer -> (k,) int64 face indices in boundary_face_order
     local_cell: dict     # peer -> (k,) int64 cell owned by `rank`
     local_side: dict     # peer -> (k,) int8
     local_fs: dict       # peer -> (k,) int8: the local cell's side slot 2*axis + s of the face
+    vpath: dict = field(default_factory=dict)    # peer -> (k, MAX_CHAIN, 2) int8 (AdaptiveMesh)
+    vdepth: dict = field(default_factory=dict)   # peer -> (k,) int8: 0 = no virtual side
     device_index: dict = field(default_factory=dict)   # (peer, device) -> (cell int32, fs int8) on the device
 
 
@@ -181,7 +192,14 @@ def exchange_plan(mesh, decomp: DomainDecomposition, rank: int) -> ExchangePlan:
         smap[q] = np.where(lo_mine, 0, 1).astype(np.int8)
         # the lo owner sees the face on its upper side (s = 1), the hi owner on its lower side
         fsmap[q] = (2 * axis[f] + np.where(lo_mine, 1, 0)).astype(np.int8)
-    return ExchangePlan(rank, peers, fmap, cmap, smap, fsmap)
+    plan = ExchangePlan(rank, peers, fmap, cmap, smap, fsmap)
+    if isinstance(mesh, AdaptiveMesh):
+        leaf = np.nonzero((mesh.face_kind != 2).all(axis=1) & (mesh.face_cell[:, 0] != mesh.face_cell[:, 1]))[0]
+        for q in peers:
+            li = leaf[fmap[q]]
+            plan.vpath[q] = mesh.face_vpath[li].copy()
+            plan.vdepth[q] = np.where((mesh.face_kind[li] == 1).any(axis=1), mesh.face_vdepth[li], 0).astype(np.int8)
+    return plan
 
 
 def pack_boundary_traces(plan: ExchangePlan, peer: int, trace_q, trace_f):

@@ -324,3 +324,22 @@ def test_gpu_sharded_step_equals_single_domain(R):
         q_sharded[cells] = out.reshape(q_single.shape)[cells]
     torch.cuda.synchronize()
     assert torch.equal(q_sharded, q_r1)              # rank-count transparency, bitwise
+
+
+def test_adaptive_plan_carries_the_chain_paths():
+    """A rank-boundary hanging face carries the leaf's interpolation path in the
+    plan, identical on both ranks (the receiver of a coarse owner's trace
+    evaluates it at the leaf's points)."""
+    G = GOLDEN["refined"]
+    cells = [_key(c) for c in G["cells"]]
+    mesh = AdaptiveMesh(cells, 2, True)
+    for R in (2, 3, 4):
+        dec = decompose(mesh, R)
+        plans = [exchange_plan(mesh, dec, r) for r in range(R)]
+        hanging = 0
+        for p in plans:
+            for q in p.peers:
+                assert np.array_equal(p.vpath[q], plans[q].vpath[p.rank])
+                assert np.array_equal(p.vdepth[q], plans[q].vdepth[p.rank])
+                hanging += int((p.vdepth[q] > 0).sum())
+        assert hanging > 0
