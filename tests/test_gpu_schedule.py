@@ -10,7 +10,9 @@ two-step graph records its first-CTA start and last-CTA exit on the device
 clock (edg_trace_next), and the SPEC's invariants are asserted on that trace:
 
 * Priority: the skeleton predictor starts no later than the
-  enclave predictor;
+  enclave predictor (within 1 us of dispatch jitter: one event releases
+  both), and the skeleton faces -- launched after the skeleton predictor,
+  while the enclave predictor occupies the GPU -- start within 3 us of it;
 * Safety: no face solve starts before the predictors of the
   cells it reads have finished; the corrector starts after every face solve;
 * Overlap (the device analogue of "sends are overlapped with
@@ -80,8 +82,13 @@ def test_schedule_invariants_in_replayed_graph(cfg5_solver, tmp_path):
             assert rs[0] >= sf[1]
             assert fa[0] >= max(sk[1], en[1], rs[1])
             assert co[0] >= fa[1]
-            # Priority
-            assert sk[0] <= en[0], f"enclave STP started {sk[0] - en[0]} ns before the skeleton STP"
+            # Priority: both predictors are released by the same event; the
+            # skeleton one is not behind (first-CTA starts within dispatch
+            # jitter), and the later high-priority launch is not queued behind
+            # the running enclave predictor (a persistent enclave grid held it
+            # back ~10 us; the background launch frees slots as CTAs retire)
+            assert sk[0] <= en[0] + 1000, f"enclave STP started {sk[0] - en[0]} ns before the skeleton STP"
+            assert sf[0] - sk[1] <= 3000, f"skeleton faces waited {sf[0] - sk[1]} ns"
             # Overlap: the skeleton phase is done while the enclave predictor runs
             assert rs[1] <= en[1], f"restriction ended {rs[1] - en[1]} ns after the enclave STP"
             assert sf[0] < en[1]
