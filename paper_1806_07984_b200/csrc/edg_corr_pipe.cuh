@@ -28,7 +28,10 @@ struct CorrPipe {
 #ifndef EDG_CORR_PIPE_TARGET
 #define EDG_CORR_PIPE_TARGET 256
 #endif
-  static constexpr int CPB = NPC >= 96 ? 1 : (EDG_CORR_PIPE_TARGET / NPC > 0 ? EDG_CORR_PIPE_TARGET / NPC : 1);
+#ifndef EDG_CORR_CPB_BIG
+#define EDG_CORR_CPB_BIG 1
+#endif
+  static constexpr int CPB = NPC >= 96 ? EDG_CORR_CPB_BIG : (EDG_CORR_PIPE_TARGET / NPC > 0 ? EDG_CORR_PIPE_TARGET / NPC : 1);
   // EDG_CORR_WIDE (default 1): with one cell per group and more face points
   // than nodes (3-D p = 4: 150 > 125), the CTA is sized for the face points so
   // that the Rusanov phase is one pass over 160 threads instead of two

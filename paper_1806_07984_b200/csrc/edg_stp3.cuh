@@ -35,6 +35,10 @@ namespace edg {
 #ifndef EDG_STP3_G
 #define EDG_STP3_G(n) ((n) <= 5 ? (n) : 3)
 #endif
+// pencil phase with one (component, pencil) per thread (n = 5; larger n spill)
+#ifndef EDG_STP3_KMAP
+#define EDG_STP3_KMAP(n) ((n) <= 5)
+#endif
 // resident CTAs per SM asked of ptxas (n = 5: 248 registers, no spills)
 #ifndef EDG_STP3_MINB
 #define EDG_STP3_MINB(n) ((n) <= 5 ? 2 : 1)
@@ -81,6 +85,10 @@ stp_picard3_kernel(const StpArgs A) {
   const int pos[DIM] = {N * (i1 * N + i2) + i0, N * (i0 * N + i2) + i1, N * (i0 * N + i1) + i2};
   const double dt = *A.dt;
   const int nblocks = A.nwork;
+  // pencil-phase map: one (component, pencil) per thread when they fill the CTA
+  constexpr bool KMAP = EDG_STP3_KMAP(N) && M * NF <= THREADS && 2 * M * NF > THREADS;
+  const bool pb_ok = tid < M * NF;
+  double* const pbase = sF + (pb_ok ? (tid / NF) * ROW + (tid % NF) * N : 0);
 
   auto prefetch_q = [&](int b, int buf) {
     if (lane_ok && b < A.nwork) {
@@ -134,6 +142,34 @@ stp_picard3_kernel(const StpArgs A) {
     };
     // B: in-place pencil contraction of the rows of group slots [0, ng)
     auto pencils = [&](int ng) {
+      if constexpr (KMAP) {
+        // thread (component k, pencil p): every row (a, g, k) of its k at its
+        // pencil -- no index arithmetic, and the warp-wide stride-n accesses
+        // of two consecutive k rows (row stride n^3) stay at two wavefronts
+        if (pb_ok) {
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) {
+            const double ih = sIh[a];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              if (g < ng) {
+                double* P = pbase + (a * G + g) * M * ROW;
+                double f[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) f[j] = P[j];
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                  double h = 0.0;
+#pragma unroll
+                  for (int j = 0; j < N; ++j) h = fma(kPen[O + EDG_BASIS_D(N) + i * N + j], f[j], h);
+                  P[i] = h * ih;
+                }
+              }
+            }
+          }
+        }
+        return;
+      }
       const int tasks = DIM * ng * M * NF;
       for (int t = tid; t < tasks; t += THREADS) {
         const int rg = t / NF, p = t - rg * NF;          // rg = (a, g, k) within the used slots
