@@ -7,8 +7,11 @@ face solve reads must hold the right global neighbour's trace -- both in one
 process and through torch.distributed (gloo, world size 2).
 GPU (marked): R = 2, 3 ranks emulated in one process (SPEC.md:500
 "interleaved" mode; the ranks' kernels never wait on one another) are
-bitwise the single-domain DGSolver run over 5 steps, and the
-torch.distributed step path (two priority streams, NCCL, world size 1) too.
+bitwise the single-domain DGSolver run over 5 steps; the torch.distributed
+step path (two priority streams) is bitwise too, with NCCL at world size 1
+and with two real ranks over gloo (host-staged exchange: neither rank's
+device work ever waits on the other's, so the two processes can share the
+one GPU).
 """
 import os
 import socket
@@ -175,3 +178,54 @@ def test_gpu_torch_distributed_step_world1():
         assert np.array_equal(s.state().cpu().numpy(), ref)
     finally:
         dist.destroy_process_group()
+
+
+def _gpu_worker(rank, world, port, q, N):
+    """One rank of a real torch.distributed sharded run (gloo: host-staged
+    exchange, so no device work of one rank ever waits on the other's)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    import paper_1806_07984_b200 as edg
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = edg.configs.CONFIGS["cfg2"].with_(cells=N, cfl=0.2)
+        mesh = CartesianMesh(N, 2, True)
+        s = edg.sharded.ShardedDGSolver(edg.pde.euler(2), cfg.order, mesh, cfg.cfl, decompose(mesh, world), rank,
+                                        comm=edg.sharded.TorchComm(dist))
+        s.set_state(edg.configs.initial_dg_uniform(cfg))
+        for _ in range(3):
+            s.step()
+        torch.cuda.synchronize()
+        s.check_status()
+        q.put((rank, s.layout.local, s.state().cpu().numpy(), s.dt_history()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_torch_distributed_world2_bitwise():
+    """Two ranks through the torch.distributed step path (priority streams,
+    per-neighbour exchange, dt slots all-reduced) reproduce the single-domain
+    run bitwise."""
+    import torch
+    import paper_1806_07984_b200 as edg
+    N = 27
+    cfg = edg.configs.CONFIGS["cfg2"].with_(cells=N, cfl=0.2)
+    ref, ref_dt = _single(edg, cfg, N, edg.configs.initial_dg_uniform(cfg), 3)
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, N)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    out = np.empty_like(ref)
+    for _ in range(2):
+        rank, local, Q, dt = q.get()
+        out[local] = Q
+        assert np.array_equal(dt, ref_dt)
+    assert np.array_equal(out, ref)
