@@ -43,20 +43,30 @@ struct CorrPipe {
   static constexpr int WORK = WIDE ? TOTF : CPB * NPC;
   static constexpr int THREADS = ((WORK + 31) / 32) * 32 < 64 ? 64 : ((WORK + 31) / 32) * 32;
   static constexpr int TRC = 2 * DIM * M * NF;            // trace doubles per cell (one family)
-  static constexpr int QE = (CPB * M * NPC + 1) & ~1;     // stage sub-blocks, even -> 16-byte aligned
+  // EDG_CORR_QEG (uniform grids, one cell per group): q_end is not staged --
+  // each thread loads its node's values straight into registers at the start
+  // of the group (5 KB less shared memory per stage on 3-D p = 4)
+#ifndef EDG_CORR_QEG
+#define EDG_CORR_QEG 1
+#endif
+  static constexpr bool QEG = EDG_CORR_QEG && GRID && CPB == 1;
+  static constexpr int QE = QEG ? 0 : (CPB * M * NPC + 1) & ~1;     // stage sub-blocks, even -> 16-byte aligned
   static constexpr int TB = (CPB * TRC + 1) & ~1;
   // grid: q_end, trace_q, trace_f, neighbour trace_q;  adaptive: q_end,
   // trace_f, face outcomes (gathered through side_face)
   static constexpr int NB = GRID ? 3 : 2;
   static constexpr int STAGE = QE + NB * TB;
   static constexpr int NV = GRID ? 2 * DIM * N : CPB * 2 * DIM * N;    // lift vectors (per cell when adaptive)
+  // resident CTAs asked of ptxas: 5 fit the shared memory of the unstaged-q_end 3-D kernel
+  static constexpr int MINB = (QEG && DIM == 3) ? 5 : 1;
   static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TB + NV) +
                                   sizeof(unsigned long long) * (1 + CPB + CPB + 2) +
                                   sizeof(unsigned) * (((2 * DIM * CPB + 1) & ~1));
 };
 
 template <int KIND, int DIM, int N, bool GRID = true>
-__global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) corrector_grid_pipe_kernel(const CorrArgs A) {
+__global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS, CorrPipe<KIND, DIM, N, GRID>::MINB)
+corrector_grid_pipe_kernel(const CorrArgs A) {
   const TraceScope trace_scope(A.trace);
   using P = Pde<KIND, DIM>;
   using C = CorrPipe<KIND, DIM, N, GRID>;
@@ -124,6 +134,7 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
     const int c0 = g * CPB;
     const int nc = min(CPB, A.ncells - c0);
     constexpr int NBK = C::NB;   // contiguous blocks: q_end, (trace_q,) trace_f
+    constexpr int B0 = C::QEG ? 1 : 0;   // q_end not staged
     const double* srcs[3] = {A.q_end + (size_t)c0 * M * NPC, GRID ? A.trace_q + (size_t)c0 * TRC : A.trace_f + (size_t)c0 * TRC,
                              A.trace_f + (size_t)c0 * TRC};
     double* dsts[3] = {st, st + C::QE, st + C::QE + C::TB};
@@ -131,7 +142,7 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
     unsigned bulk_bytes = 0;
     bool bulk[3] = {false, false, false};
 #pragma unroll
-    for (int i = 0; i < NBK; ++i) {
+    for (int i = B0; i < NBK; ++i) {
       bulk[i] = ((reinterpret_cast<uintptr_t>(srcs[i]) & 15) == 0) && ((cnt[i] * 8) % 16 == 0);
       if (bulk[i]) bulk_bytes += (unsigned)cnt[i] * 8u;
     }
@@ -144,13 +155,13 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
     if constexpr (GRID && (BLK * 8) % 16 == 0 && (TRC * 8) % 16 == 0) {
       bool all = (reinterpret_cast<uintptr_t>(A.trace_q) & 15) == 0;
 #pragma unroll
-      for (int i = 0; i < NBK; ++i) all = all && bulk[i];
+      for (int i = B0; i < NBK; ++i) all = all && bulk[i];
       if (all) {
         if (tid == 0) mbar_expect_tx(bar, bulk_bytes + (unsigned)(nc * 2 * DIM * BLK * 8));
         __syncthreads();
         if (tid == 0) {
 #pragma unroll
-          for (int i = 0; i < NBK; ++i) bulk_g2s(dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
+          for (int i = B0; i < NBK; ++i) bulk_g2s(dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
         }
         double* nq = st + C::QE + (C::NB - 1) * C::TB;
         for (int bi = tid; bi < nc * 2 * DIM; bi += THREADS) {
@@ -173,11 +184,11 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
     if (tid == 0) {
       mbar_arrive_expect_tx(bar, bulk_bytes);
 #pragma unroll
-      for (int i = 0; i < NBK; ++i)
+      for (int i = B0; i < NBK; ++i)
         if (bulk[i]) bulk_g2s(dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
     }
 #pragma unroll
-    for (int i = 0; i < NBK; ++i)
+    for (int i = B0; i < NBK; ++i)
       if (!bulk[i]) cp_block<THREADS>(dsts[i], srcs[i], cnt[i], tid);
     double* nq = st + C::QE + (C::NB - 1) * C::TB;
     constexpr int NW = THREADS / 32;
@@ -245,6 +256,13 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
     const bool has_cell = slot < CPB && cell < A.ncells;
     const bool cell_ok = g * CPB < A.ncells;   // (WIDE: one cell, every thread in phase 1)
     const double* qe = cur;
+    // QEG: this node's q_end straight from global memory, issued before the
+    // face phase so the loads overlap it
+    double qeg[M];
+    if constexpr (C::QEG) {
+#pragma unroll
+      for (int k = 0; k < M; ++k) qeg[k] = has_cell ? __ldg(A.q_end + (size_t)cell * M * NPC + (size_t)k * NPC + node) : 0.0;
+    }
     const double* tq = cur + C::QE;
     const double* tf = cur + C::QE + (GRID ? C::TB : 0);
     const double* nq = cur + C::QE + (C::NB - 1) * C::TB;
@@ -294,7 +312,7 @@ __global__ void __launch_bounds__(CorrPipe<KIND, DIM, N, GRID>::THREADS) correct
     double qn[M];
     bool finite = true;
 #pragma unroll
-    for (int k = 0; k < M; ++k) qn[k] = has_cell ? qe[(slot * M + k) * NPC + node] : 0.0;
+    for (int k = 0; k < M; ++k) qn[k] = C::QEG ? qeg[k] : (has_cell ? qe[(slot * M + k) * NPC + node] : 0.0);
     if (has_cell) {
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {

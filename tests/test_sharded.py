@@ -220,12 +220,12 @@ def test_gpu_torch_distributed_world2_bitwise():
     procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, N)) for r in range(2)]
     for p in procs:
         p.start()
+    res = [q.get() for _ in range(2)]     # before join: the payloads exceed the pipe buffer
     for p in procs:
         p.join(300)
         assert p.exitcode == 0
     out = np.empty_like(ref)
-    for _ in range(2):
-        rank, local, Q, dt = q.get()
+    for rank, local, Q, dt in res:
         out[local] = Q
         assert np.array_equal(dt, ref_dt)
     assert np.array_equal(out, ref)
