@@ -215,12 +215,12 @@ def test_gpu_torch_distributed_world2_bitwise():
     cfg = edg.configs.CONFIGS["cfg2"].with_(cells=N, cfl=0.2)
     ref, ref_dt = _single(edg, cfg, N, edg.configs.initial_dg_uniform(cfg), 3)
     ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
+    q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, N)) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get() for _ in range(2)]     # before join: the payloads exceed the pipe buffer
+    res = [q.get(timeout=300) for _ in range(2)]     # before join: the payloads exceed the pipe buffer
     for p in procs:
         p.join(300)
         assert p.exitcode == 0
