@@ -147,6 +147,17 @@ int edg_corrector_grid(const edg_pde* pde, int32_t order, const double* basis_de
                        unsigned long long* dt_slots_dev, const double* hmin_dev, uint32_t* status_dev,
                        void* stream);
 
+/* The same on the cells [cell_begin, cell_begin + cell_count) of the grid
+ * (cell_count < 0: to the end).  Neighbour traces are read wherever they lie,
+ * so the predictor outputs of the adjacent cells must be complete; used by the
+ * slab-streamed host step (solver.DGSolver.step_host), which corrects slab j
+ * as soon as the predictor of slab j + 1 is done. */
+int edg_corrector_grid_range(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t cells_per_axis,
+                             int32_t periodic, int32_t cell_begin, int32_t cell_count, const double* q_end_dev,
+                             const double* trace_q_dev, const double* trace_f_dev, const double* edges_dev,
+                             double* q_out_dev, unsigned long long* dt_slots_dev, const double* hmin_dev,
+                             uint32_t* status_dev, void* stream);
+
 /* ---- admissible_dt (kernels.py:267-281) -----------------------------------
  * edg_cell_speed_reduce: per-cell lambda (max over axes of max over nodes,
  * NaN axes dropped like Python max) -> candidate h_c / ((2p+1) lambda_c) for

@@ -45,6 +45,7 @@ SIGNATURES = {
     "edg_riemann_rusanov": (C.c_int, [PDEP, I32, I32, P, P, I32, I32, P, P]),
     "edg_corrector": (C.c_int, [PDEP, I32, P, I32, P, P, P, P, P, P, P, I32, P, P, P, P, P]),
     "edg_corrector_grid": (C.c_int, [PDEP, I32, P, I32, I32, P, P, P, P, P, P, P, P, P]),
+    "edg_corrector_grid_range": (C.c_int, [PDEP, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P]),
     "edg_cell_speed_reduce": (C.c_int, [PDEP, I32, I32, I32, P, P, I32, P, P]),
     "edg_dt_slots_reset": (C.c_int, [P, P]),
     "edg_dt_finalize": (C.c_int, [P, D, P, P, I32, P, P]),

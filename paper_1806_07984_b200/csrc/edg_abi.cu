@@ -221,6 +221,7 @@ int edg_corrector(const edg_pde* pde, int32_t order, const double* basis_dev, in
   CorrArgs a;
   a.basis = basis_dev;
   a.ncells = ncells;
+  a.cell_base = 0;
   a.order = order;
   a.q_end = q_end_dev;
   a.trace_q = trace_q_dev;
@@ -245,6 +246,15 @@ int edg_corrector_grid(const edg_pde* pde, int32_t order, const double* basis_de
                        int32_t periodic, const double* q_end_dev, const double* trace_q_dev, const double* trace_f_dev,
                        const double* edges_dev, double* q_out_dev, unsigned long long* dt_slots_dev,
                        const double* hmin_dev, uint32_t* status_dev, void* stream) {
+  return edg_corrector_grid_range(pde, order, basis_dev, cells_per_axis, periodic, 0, -1, q_end_dev, trace_q_dev,
+                                  trace_f_dev, edges_dev, q_out_dev, dt_slots_dev, hmin_dev, status_dev, stream);
+}
+
+int edg_corrector_grid_range(const edg_pde* pde, int32_t order, const double* basis_dev, int32_t cells_per_axis,
+                             int32_t periodic, int32_t cell_begin, int32_t cell_count, const double* q_end_dev,
+                             const double* trace_q_dev, const double* trace_f_dev, const double* edges_dev,
+                             double* q_out_dev, unsigned long long* dt_slots_dev, const double* hmin_dev,
+                             uint32_t* status_dev, void* stream) {
   unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
@@ -254,9 +264,13 @@ int edg_corrector_grid(const edg_pde* pde, int32_t order, const double* basis_de
   long long nc = 1;
   for (int d = 0; d < pde->dim; ++d) nc *= cells_per_axis;
   if (nc > 0x7fffffffLL) return fail(EDG_ERR_CONFIG, "grid too large");
+  if (cell_count < 0) cell_count = (int32_t)(nc - cell_begin);
+  if (cell_begin < 0 || (long long)cell_begin + cell_count > nc) return fail(EDG_ERR_CONFIG, "cell range outside the grid");
+  if (cell_count == 0) return EDG_OK;
   CorrArgs a;
   a.basis = basis_dev;
-  a.ncells = (int32_t)nc;
+  a.ncells = cell_begin + cell_count;
+  a.cell_base = cell_begin;
   a.order = order;
   a.q_end = q_end_dev;
   a.trace_q = trace_q_dev;

@@ -88,7 +88,7 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
   const int slot = tid / NPC;
   const int node = tid - slot * NPC;
   const int n = A.grid_n;
-  const int ngroups = (A.ncells + CPB - 1) / CPB;
+  const int ngroups = (A.ncells - A.cell_base + CPB - 1) / CPB;   // cells [cell_base, ncells)
 
   // lift vectors v[a][s][i] = (sign * l_i(s)) / (w_i * h_a)   (kernels.py:190-191)
   auto lift = [&](int i, const double* e) {
@@ -131,7 +131,7 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
   // 16-byte aligned and sized (one instruction each, completion counted on
   // the stage's mbarrier); otherwise cooperative cp.async.
   auto load_group = [&](int g, double* st, unsigned long long* bar) {
-    const int c0 = g * CPB;
+    const int c0 = A.cell_base + g * CPB;
     const int nc = min(CPB, A.ncells - c0);
     constexpr int NBK = C::NB;   // contiguous blocks: q_end, (trace_q,) trace_f
     constexpr int B0 = C::QEG ? 1 : 0;   // q_end not staged
@@ -252,9 +252,9 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
     mbar_wait(sBar + (it & 1), (it >> 1) & 1);  // bulk copies of this group
     __syncthreads();
 
-    const int cell = g * CPB + slot;
+    const int cell = A.cell_base + g * CPB + slot;
     const bool has_cell = slot < CPB && cell < A.ncells;
-    const bool cell_ok = g * CPB < A.ncells;   // (WIDE: one cell, every thread in phase 1)
+    const bool cell_ok = A.cell_base + g * CPB < A.ncells;   // (WIDE: one cell, every thread in phase 1)
     const double* qe = cur;
     // QEG: this node's q_end straight from global memory, issued before the
     // face phase so the loads overlap it
@@ -270,7 +270,7 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
       // per-cell lift vectors of this group (cell edges may differ)
       for (int i = tid; i < CPB * 2 * DIM * N; i += THREADS) {
         const int sl = i / (2 * DIM * N);
-        const int c = g * CPB + sl;
+        const int c = A.cell_base + g * CPB + sl;
         if (c < A.ncells) sV[i] = lift(i - sl * 2 * DIM * N, A.edges + (A.edges_per_cell ? (size_t)c * DIM : 0));
       }
     }
@@ -362,7 +362,7 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
       seg_max_redux(sLamC, has_cell ? slot : -1, segmask, (unsigned long long)__double_as_longlong(lam));
       __syncthreads();
       if (tid < CPB) {
-        const int c = g * CPB + tid;
+        const int c = A.cell_base + g * CPB + tid;
         const double lc = __longlong_as_double((long long)sLamC[tid]);
         if (c < A.ncells && lc > 0.0) {
           const unsigned long long cand = (unsigned long long)__double_as_longlong(
@@ -373,7 +373,7 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
       }
     }
     if (tid < CPB) {
-      const int c = g * CPB + tid;
+      const int c = A.cell_base + g * CPB + tid;
       if (c < A.ncells && sFlag[tid]) ++nonfinite;
       sFlag[tid] = 0ull;
       // the other parity's flags are next written after this group's barriers

@@ -18,7 +18,8 @@ namespace edg {
 
 struct CorrArgs {
   const double* basis;
-  int32_t ncells;
+  int32_t ncells;           // end of the cell range (exclusive)
+  int32_t cell_base;        // first cell of the range (0: all cells)
   int32_t order;
   const double* q_end;
   const double* trace_q;
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
   const int tid = threadIdx.x;
   const int slot = tid / NPC;
   const int node = tid - slot * NPC;
-  const int cell = blockIdx.x * CPB + slot;
+  const int cell = A.cell_base + blockIdx.x * CPB + slot;   // cells [cell_base, ncells)
   const bool has_cell = slot < CPB && cell < A.ncells;
 
   if (tid < CPB * DIM) sLam[tid] = 0ull;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
       __syncthreads();
       if (tid < CPB) {
         unsigned long long best = DT_EMPTY;
-        const int c = blockIdx.x * CPB + tid;
+        const int c = A.cell_base + blockIdx.x * CPB + tid;
         if (c < A.ncells) {
           const double lc = __longlong_as_double((long long)sLam[tid]);
           if (lc > 0.0) best = (unsigned long long)__double_as_longlong(dt_candidate(A.hmin[c], A.order, lc));

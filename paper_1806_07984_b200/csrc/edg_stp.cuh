@@ -118,7 +118,11 @@ struct StpCfg {
 #ifndef EDG_STP_MINB_2D
 #define EDG_STP_MINB_2D 3
 #endif
-  static constexpr int MINB = DIM == 2 ? EDG_STP_MINB_2D : EDG_STP_MINB_3D;
+  // 2-D n = 4 (cfg5's p = 3): its own cap (A/B: EDG_STP_MINB_2D_N4)
+#ifndef EDG_STP_MINB_2D_N4
+#define EDG_STP_MINB_2D_N4 5   // 128 registers, 5 CTAs per SM: cfg5 graph step 48.2 -> 46.4 us
+#endif
+  static constexpr int MINB = DIM == 2 ? (N == 4 ? EDG_STP_MINB_2D_N4 : EDG_STP_MINB_2D) : EDG_STP_MINB_3D;
 };
 
 template <int KIND, int DIM, int N>

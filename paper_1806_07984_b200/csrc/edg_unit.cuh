@@ -170,7 +170,7 @@ static int launch_corr_n(bool fused, const CorrArgs& a, cudaStream_t st) {
     if (set_smem(kern, C::BYTES)) return EDG_ERR_CUDA;
     const int grid_cap = persistent_grid(kern, C::THREADS, C::BYTES);
     if (grid_cap < 0) return EDG_ERR_CUDA;
-    const int ngroups = (a.ncells + C::CPB - 1) / C::CPB;
+    const int ngroups = (a.ncells - a.cell_base + C::CPB - 1) / C::CPB;
     if (ngroups > grid_cap) {
       kern<<<grid_cap, C::THREADS, C::BYTES, st>>>(a);
       return check_launch();
@@ -181,7 +181,7 @@ static int launch_corr_n(bool fused, const CorrArgs& a, cudaStream_t st) {
   // cfg5, whose 13k cells give each persistent CTA about one group)
   using Cf = CorrCfg<DIM, N>;
   const size_t smem = CorrSmem<KIND, DIM, N>::BYTES;
-  const int blocks = (a.ncells + Cf::CPB - 1) / Cf::CPB;
+  const int blocks = (a.ncells - a.cell_base + Cf::CPB - 1) / Cf::CPB;
   if (blocks <= 0) return EDG_OK;
   if (fused) {
     auto kern = corrector_kernel<KIND, DIM, N, true>;

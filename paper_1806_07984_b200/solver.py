@@ -161,6 +161,7 @@ class _Base:
         consecutive steps are captured once into a CUDA graph and replayed
         (chunk must be even so the double buffers return to their roles)."""
         torch = self.torch
+        self._state_gen = getattr(self, "_state_gen", 0) + 1
         if not graph:
             for _ in range(steps):
                 self.step()
@@ -221,6 +222,7 @@ class _Base:
         self._graph_steps, self._graph_key = chunk, key
 
     def step(self):
+        self._state_gen = getattr(self, "_state_gen", 0) + 1
         self._enqueue_step()
         self.steps_done += 1
 
@@ -329,6 +331,7 @@ class DGSolver(_Base):
         src = Q if isinstance(Q, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(Q, dtype=np.float64))
         self.Q.copy_(src.reshape(self.Q.shape), non_blocking=True)
         self.steps_done = 0
+        self._state_gen = getattr(self, "_state_gen", 0) + 1
         self.status.zero_()
         self._seed_dt()
 
@@ -343,6 +346,132 @@ class DGSolver(_Base):
 
     def state(self):
         return self.Q
+
+    # ------------------------------------------------- host-resident steps --
+    def step_host(self, q_in, q_out, slabs: int = 16):
+        """One step from a host state to a host buffer (the drop-in use of
+        the reference's numpy API, where every call takes and returns host
+        arrays), streamed in slabs of the uniform grid so that the PCIe
+        transfers overlap each other and the kernels:
+
+            copy-in stream : H2D slab j                         (waits D2H slab j of the previous call)
+            compute stream : dt candidates of slab j (as it lands) -> dt = cfl * min
+                             -> per slab: Picard order, predictor(slab j),
+                                corrector(slab j - 1) once predictor(j) is done
+            copy-out stream: D2H slab j after its corrector
+
+        A slab is a run of whole axis-0 layers, so a cell's face neighbours
+        lie in its own or the adjacent slab; on a periodic grid slab 0 is
+        corrected last (its lower neighbour is the last slab).  dt is the
+        admissible step of q_in itself (kernels.py:267-281), reduced on the
+        device as the slabs arrive, so the result is bitwise that of
+        set_state(q_in); step().  q_in / q_out: CPU tensors of the state's
+        shape (pinned for asynchronous copies).  q_out is complete when the
+        event `host_ready` has completed (host_wait() makes the current
+        stream wait for it); the current stream itself does not wait, so the
+        next call's uploads overlap this call's downloads."""
+        torch = self.torch
+        if self.adaptive:
+            raise ConfigError("step_host streams uniform grids only")
+        lib = self.lib
+        m, d = self.pde.m, self.pde.dim
+        N = self.mesh.N
+        layer = N ** (d - 1)
+        S = max(1, min(int(slabs), N))
+        bounds = [(N * j // S) * layer for j in range(S + 1)]
+        if not hasattr(self, "_sh"):
+            self._sh = {"in": torch.cuda.Stream(), "out": torch.cuda.Stream(), "prev_out": {},
+                        "order": torch.zeros(self.ncells, dtype=torch.int32, device="cuda")}
+        sh = self._sh
+        if sh["order"].numel() < self.ncells:
+            sh["order"] = torch.zeros(self.ncells, dtype=torch.int32, device="cuda")
+        src = q_in.reshape(self.Q.shape)
+        dst = q_out.reshape(self.Q.shape)
+        main = torch.cuda.current_stream()
+        Q, Qn = self.Q, self.Qn
+        npts = self.basis.n ** d
+        ev_in = []
+        if sh.get("gen") != getattr(self, "_state_gen", 0):
+            # other work on the state since the last step_host: the uploads
+            # wait for everything enqueued on the current stream; back-to-back
+            # calls only wait per slab for the previous call's download
+            sh["in"].wait_stream(main)
+            sh["prev_out"] = {}
+        _lib.check(lib.edg_dt_slots_reset(_lib.ptr(self.slots), _stream()), "dt reset")
+        for j in range(S):
+            c0, c1 = bounds[j], bounds[j + 1]
+            with torch.cuda.stream(sh["in"]):
+                prev = sh["prev_out"].get((c0, c1))
+                if prev is not None:
+                    sh["in"].wait_event(prev)     # host / device slab still being read by the last call's copy-out
+                Q[c0:c1].copy_(src[c0:c1], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(sh["in"])
+            ev_in.append(e)
+            main.wait_event(e)
+            _lib.check(lib.edg_cell_speed_reduce(C.byref(self.native), self.order, c1 - c0, npts, _lib.ptr(Q[c0:c1]),
+                                                 _lib.ptr(self.hmin), 0, _lib.ptr(self.slots), _stream()),
+                       "admissible_dt")
+        self._finalize_dt()
+        order = sh["order"]
+        corr_order = list(range(S))
+        if self.mesh.periodic and S > 1:
+            corr_order = corr_order[1:] + [0]      # slab 0 reads the last slab's traces
+        done_stp = set()
+        pending = list(corr_order)
+        prev_out = {}
+
+        def corrector(j):
+            c0, c1 = bounds[j], bounds[j + 1]
+            self._trace("Corrector")
+            _lib.check(lib.edg_corrector_grid_range(C.byref(self.native), self.order, _lib.ptr(self.table), N,
+                                                    int(self.mesh.periodic), c0, c1 - c0, _lib.ptr(self.q_end),
+                                                    _lib.ptr(self.trace_q), _lib.ptr(self.trace_f),
+                                                    _lib.ptr(self.edges), _lib.ptr(Qn), _lib.ptr(self.slots),
+                                                    _lib.ptr(self.hmin), _lib.ptr(self.status), _stream()),
+                       "corrector")
+            e = torch.cuda.Event()
+            e.record(main)
+            with torch.cuda.stream(sh["out"]):
+                sh["out"].wait_event(e)
+                dst[c0:c1].copy_(Qn[c0:c1], non_blocking=True)
+                eo = torch.cuda.Event()
+                eo.record(sh["out"])
+            prev_out[(c0, c1)] = eo
+
+        def ready(j):
+            need = {j - 1, j, j + 1} if not self.mesh.periodic else {(j - 1) % S, j, (j + 1) % S}
+            return all(x in done_stp for x in need if 0 <= x < S)
+
+        for j in range(S):
+            c0, c1 = bounds[j], bounds[j + 1]
+            nc = c1 - c0
+            _lib.check(lib.edg_order_by_iterations(nc, _lib.ptr(self.iterations[c0:c1]), _lib.ptr(order[c0:c1]),
+                                                   _lib.ptr(self.order_scratch), _stream()), "order")
+            self._trace("STP")
+            _lib.check(lib.edg_stp_picard(C.byref(self.native), self.order, _lib.ptr(self.table), _lib.ptr(Q[c0:c1]),
+                                          _lib.ptr(order[c0:c1]), nc, _lib.ptr(self.edges), 0, _lib.ptr(self.dt),
+                                          self.tol, self.max_iter, _lib.ptr(self.q_end[c0:c1]), None,
+                                          _lib.ptr(self.trace_q[c0:c1]), _lib.ptr(self.trace_f[c0:c1]),
+                                          _lib.ptr(self.iterations[c0:c1]), _lib.ptr(self.converged[c0:c1]),
+                                          _lib.ptr(self.iter_total), _stream()), "stp_picard")
+            done_stp.add(j)
+            while pending and ready(pending[0]):
+                corrector(pending.pop(0))
+        while pending:
+            corrector(pending.pop(0))
+        sh["prev_out"] = prev_out
+        sh["gen"] = getattr(self, "_state_gen", 0)
+        self.host_ready = torch.cuda.Event()
+        self.host_ready.record(sh["out"])
+        self.Q, self.Qn = self.Qn, self.Q
+        self.steps_done += 1
+
+    def host_wait(self):
+        """Make the current stream wait for the last step_host's downloads."""
+        ev = getattr(self, "host_ready", None)
+        if ev is not None:
+            self.torch.cuda.current_stream().wait_event(ev)
 
     # ----------------------------------------------------------------- step --
     def _worker(self):
@@ -492,6 +621,7 @@ class FVSolver(_Base):
         src = P if isinstance(P, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(P, dtype=np.float64))
         self.Q.copy_(src.reshape(self.Q.shape), non_blocking=True)
         self.steps_done = 0
+        self._state_gen = getattr(self, "_state_gen", 0) + 1
         self.status.zero_()
         _lib.check(self.lib.edg_dt_slots_reset(_lib.ptr(self.slots), _stream()), "dt reset")
         _lib.check(self.lib.edg_cell_speed_reduce(C.byref(self.native), 0, self.npatches, self.k ** self.pde.dim,
