@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--cfl", type=float, default=None, help="override the config's CFL safety")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-slabs", type=int, default=None, help="slabs of the streamed host step (default: step_host's)")
+    ap.add_argument("--e2e-only", action="store_true", help="A/B helper: print only the e2e object")
     ap.add_argument("--no-variant", action="store_true", help="skip the parity-safe CFL 0.2 variant line item")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -539,7 +541,11 @@ def run_ours(args, cfg):
         del v
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(r["solver"], r["Q0"], r["dof"], args.steps, ws, dist, dev)
+        e2e = measure_e2e(r["solver"], r["Q0"], r["dof"], args.steps, ws, dist, dev, args.e2e_slabs)
+        if args.e2e_only:
+            if rank == 0:
+                print(json.dumps({"e2e": e2e, "slabs": args.e2e_slabs}))
+            return
     schedule = None
     if cfg.kind == "dg-amr":
         schedule = measure_schedule(cfg, args.steps, args.warmup)
@@ -655,7 +661,7 @@ def measure_secondary(ws, dist, dev, peak64, local):
     return out
 
 
-def measure_e2e(solver, Q0, dof, steps, ws, dist, dev):
+def measure_e2e(solver, Q0, dof, steps, ws, dist, dev, slabs=None):
     """Public API with host buffers: every step uploads the state from pinned
     host memory (set_state), advances one step, downloads the result."""
     import torch
@@ -668,7 +674,7 @@ def measure_e2e(solver, Q0, dof, steps, ws, dist, dev):
         if streamed:
             # host state in, host state out, slabs streamed (uploads, kernels
             # and downloads overlapped; dt reduced from the uploaded state)
-            solver.step_host(src, dst)
+            solver.step_host(src, dst, **({} if slabs is None else {"slabs": slabs}))
         else:
             solver.set_state(src)
             solver.step()
