@@ -347,6 +347,59 @@ class DGSolver(_Base):
     def state(self):
         return self.Q
 
+    # ------------------------------------------------------- slab helpers --
+    def _slab_bounds(self, slabs):
+        """Cell ranges of `slabs` runs of whole axis-0 layers (uniform grid)."""
+        N, d = self.mesh.N, self.pde.dim
+        S = max(1, min(int(slabs), N))
+        layer = N ** (d - 1)
+        return [(N * j // S) * layer for j in range(S + 1)]
+
+    def _slab_order_stp(self, Q, order, c0, c1, background=False, entity="STP"):
+        """Picard order of cells [c0, c1) by their last iteration counts,
+        then the predictor over them (slab-local indices, offset buffers)."""
+        lib, nc = self.lib, c1 - c0
+        _lib.check(lib.edg_order_by_iterations(nc, _lib.ptr(self.iterations[c0:c1]), _lib.ptr(order[c0:c1]),
+                                               _lib.ptr(self.order_scratch), _stream()), "order")
+        self._trace(entity)
+        fn = lib.edg_stp_picard_background if background else lib.edg_stp_picard
+        _lib.check(fn(C.byref(self.native), self.order, _lib.ptr(self.table), _lib.ptr(Q[c0:c1]),
+                      _lib.ptr(order[c0:c1]), nc, _lib.ptr(self.edges), 0, _lib.ptr(self.dt), self.tol,
+                      self.max_iter, _lib.ptr(self.q_end[c0:c1]), None, _lib.ptr(self.trace_q[c0:c1]),
+                      _lib.ptr(self.trace_f[c0:c1]), _lib.ptr(self.iterations[c0:c1]),
+                      _lib.ptr(self.converged[c0:c1]), _lib.ptr(self.iter_total), _stream()), "stp_picard")
+
+    def _slab_corrector(self, Qn, c0, c1):
+        self._trace("Corrector")
+        _lib.check(self.lib.edg_corrector_grid_range(
+            C.byref(self.native), self.order, _lib.ptr(self.table), self.mesh.N, int(self.mesh.periodic), c0, c1 - c0,
+            _lib.ptr(self.q_end), _lib.ptr(self.trace_q), _lib.ptr(self.trace_f), _lib.ptr(self.edges), _lib.ptr(Qn),
+            _lib.ptr(self.slots), _lib.ptr(self.hmin), _lib.ptr(self.status), _stream()), "corrector")
+
+    def _corrector_schedule(self, S):
+        """[(slab whose predictor completes, [slabs correctable right after])]:
+        slab j reads the traces of slabs j - 1 and j + 1 (wrapping on a
+        periodic grid, where slab 0 is corrected last)."""
+        per = self.mesh.periodic and S > 1
+        pending = list(range(1, S)) + [0] if per else list(range(S))
+        done, out = set(), []
+        for j in range(S):
+            done.add(j)
+            ready = []
+            while pending:
+                c = pending[0]
+                need = {(c - 1) % S, c, (c + 1) % S} if per else {x for x in (c - 1, c, c + 1) if 0 <= x < S}
+                if not need <= done:
+                    break
+                ready.append(pending.pop(0))
+            out.append((j, ready))
+        return out
+
+    def _slab_order_buf(self):
+        if getattr(self, "_slab_order", None) is None or self._slab_order.numel() < self.ncells:
+            self._slab_order = self.torch.zeros(self.ncells, dtype=self.torch.int32, device="cuda")
+        return self._slab_order
+
     # ------------------------------------------------- host-resident steps --
     def step_host(self, q_in, q_out, slabs: int = 16):
         """One step from a host state to a host buffer (the drop-in use of
@@ -374,23 +427,17 @@ class DGSolver(_Base):
         if self.adaptive:
             raise ConfigError("step_host streams uniform grids only")
         lib = self.lib
-        m, d = self.pde.m, self.pde.dim
-        N = self.mesh.N
-        layer = N ** (d - 1)
-        S = max(1, min(int(slabs), N))
-        bounds = [(N * j // S) * layer for j in range(S + 1)]
+        bounds = self._slab_bounds(slabs)
+        S = len(bounds) - 1
         if not hasattr(self, "_sh"):
-            self._sh = {"in": torch.cuda.Stream(), "out": torch.cuda.Stream(), "prev_out": {},
-                        "order": torch.zeros(self.ncells, dtype=torch.int32, device="cuda")}
+            self._sh = {"in": torch.cuda.Stream(), "out": torch.cuda.Stream(), "prev_out": {}}
         sh = self._sh
-        if sh["order"].numel() < self.ncells:
-            sh["order"] = torch.zeros(self.ncells, dtype=torch.int32, device="cuda")
+        order = self._slab_order_buf()
         src = q_in.reshape(self.Q.shape)
         dst = q_out.reshape(self.Q.shape)
         main = torch.cuda.current_stream()
         Q, Qn = self.Q, self.Qn
-        npts = self.basis.n ** d
-        ev_in = []
+        npts = self.basis.n ** self.pde.dim
         if sh.get("gen") != getattr(self, "_state_gen", 0):
             # other work on the state since the last step_host: the uploads
             # wait for everything enqueued on the current stream; back-to-back
@@ -407,59 +454,25 @@ class DGSolver(_Base):
                 Q[c0:c1].copy_(src[c0:c1], non_blocking=True)
                 e = torch.cuda.Event()
                 e.record(sh["in"])
-            ev_in.append(e)
             main.wait_event(e)
             _lib.check(lib.edg_cell_speed_reduce(C.byref(self.native), self.order, c1 - c0, npts, _lib.ptr(Q[c0:c1]),
                                                  _lib.ptr(self.hmin), 0, _lib.ptr(self.slots), _stream()),
                        "admissible_dt")
         self._finalize_dt()
-        order = sh["order"]
-        corr_order = list(range(S))
-        if self.mesh.periodic and S > 1:
-            corr_order = corr_order[1:] + [0]      # slab 0 reads the last slab's traces
-        done_stp = set()
-        pending = list(corr_order)
         prev_out = {}
-
-        def corrector(j):
-            c0, c1 = bounds[j], bounds[j + 1]
-            self._trace("Corrector")
-            _lib.check(lib.edg_corrector_grid_range(C.byref(self.native), self.order, _lib.ptr(self.table), N,
-                                                    int(self.mesh.periodic), c0, c1 - c0, _lib.ptr(self.q_end),
-                                                    _lib.ptr(self.trace_q), _lib.ptr(self.trace_f),
-                                                    _lib.ptr(self.edges), _lib.ptr(Qn), _lib.ptr(self.slots),
-                                                    _lib.ptr(self.hmin), _lib.ptr(self.status), _stream()),
-                       "corrector")
-            e = torch.cuda.Event()
-            e.record(main)
-            with torch.cuda.stream(sh["out"]):
-                sh["out"].wait_event(e)
-                dst[c0:c1].copy_(Qn[c0:c1], non_blocking=True)
-                eo = torch.cuda.Event()
-                eo.record(sh["out"])
-            prev_out[(c0, c1)] = eo
-
-        def ready(j):
-            need = {j - 1, j, j + 1} if not self.mesh.periodic else {(j - 1) % S, j, (j + 1) % S}
-            return all(x in done_stp for x in need if 0 <= x < S)
-
-        for j in range(S):
-            c0, c1 = bounds[j], bounds[j + 1]
-            nc = c1 - c0
-            _lib.check(lib.edg_order_by_iterations(nc, _lib.ptr(self.iterations[c0:c1]), _lib.ptr(order[c0:c1]),
-                                                   _lib.ptr(self.order_scratch), _stream()), "order")
-            self._trace("STP")
-            _lib.check(lib.edg_stp_picard(C.byref(self.native), self.order, _lib.ptr(self.table), _lib.ptr(Q[c0:c1]),
-                                          _lib.ptr(order[c0:c1]), nc, _lib.ptr(self.edges), 0, _lib.ptr(self.dt),
-                                          self.tol, self.max_iter, _lib.ptr(self.q_end[c0:c1]), None,
-                                          _lib.ptr(self.trace_q[c0:c1]), _lib.ptr(self.trace_f[c0:c1]),
-                                          _lib.ptr(self.iterations[c0:c1]), _lib.ptr(self.converged[c0:c1]),
-                                          _lib.ptr(self.iter_total), _stream()), "stp_picard")
-            done_stp.add(j)
-            while pending and ready(pending[0]):
-                corrector(pending.pop(0))
-        while pending:
-            corrector(pending.pop(0))
+        for j, ready in self._corrector_schedule(S):
+            self._slab_order_stp(Q, order, bounds[j], bounds[j + 1])
+            for c in ready:
+                c0, c1 = bounds[c], bounds[c + 1]
+                self._slab_corrector(Qn, c0, c1)
+                e = torch.cuda.Event()
+                e.record(main)
+                with torch.cuda.stream(sh["out"]):
+                    sh["out"].wait_event(e)
+                    dst[c0:c1].copy_(Qn[c0:c1], non_blocking=True)
+                    eo = torch.cuda.Event()
+                    eo.record(sh["out"])
+                prev_out[(c0, c1)] = eo
         sh["prev_out"] = prev_out
         sh["gen"] = getattr(self, "_state_gen", 0)
         self.host_ready = torch.cuda.Event()

@@ -91,3 +91,4 @@ def test_step_host_rejects_adaptive(edg):
     s = edg.solver.DGSolver(edg.pde.euler(2), 3, mesh, 0.2)
     with pytest.raises(ConfigError):
         s.step_host(None, None)
+
