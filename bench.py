@@ -668,7 +668,7 @@ def measure_e2e(solver, Q0, dof, steps, ws, dist, dev, slabs=None):
     host = torch.from_numpy(np.ascontiguousarray(Q0)).pin_memory()
     out = torch.empty_like(host).pin_memory()
     nb = host.numel() * 8
-    streamed = hasattr(solver, "step_host") and not getattr(solver, "adaptive", True)
+    streamed = hasattr(solver, "step_host") and not getattr(solver, "adaptive", False)
 
     def one(src, dst):
         if streamed:
@@ -697,7 +697,7 @@ def measure_e2e(solver, Q0, dof, steps, ws, dist, dev, slabs=None):
     b.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(dist, a.elapsed_time(b), dev)
-    api = ("DGSolver.step_host(pinned host in, pinned host out): slab-streamed H2D / predictor / corrector / D2H, "
+    api = (f"{type(solver).__name__}.step_host(pinned host in, pinned host out): slab-streamed H2D / kernels / D2H, "
            "dt from the uploaded state" if streamed else
            "set_state(pinned host) + step() + copy to pinned host")
     return {"value": dof * steps * ws / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nb,

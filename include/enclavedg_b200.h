@@ -223,6 +223,15 @@ int edg_fv_patch_step(const edg_pde* pde, int32_t k, int32_t npatches, const dou
 int edg_fv_grid_step(const edg_pde* pde, int32_t k, int32_t patches_per_axis, int32_t periodic,
                      const double* patch_dev, const double* dt_dev, const double* edges_dev, double* out_dev,
                      unsigned long long* dt_slots_dev, double h_cell, uint32_t* status_dev, void* stream);
+
+/* The same on the patches [patch_begin, patch_begin + patch_count) of the
+ * grid (patch_count < 0: to the end); halos are read from the neighbour
+ * patches of the input wherever they lie.  One slab of the streamed host step
+ * (solver.FVSolver.step_host). */
+int edg_fv_grid_step_range(const edg_pde* pde, int32_t k, int32_t patches_per_axis, int32_t periodic,
+                           int32_t patch_begin, int32_t patch_count, const double* patch_dev, const double* dt_dev,
+                           const double* edges_dev, double* out_dev, unsigned long long* dt_slots_dev, double h_cell,
+                           uint32_t* status_dev, void* stream);
 /* patch_boundary_layers (kernels.py:256-264): out (B, 2d, m, k^(d-1)). */
 int edg_patch_boundary_layers(int32_t dim, int32_t m, int32_t k, int32_t npatches,
                               const double* patch_dev, double* out_dev, void* stream);

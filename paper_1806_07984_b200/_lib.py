@@ -56,6 +56,7 @@ SIGNATURES = {
     "edg_fv_patch_update": (C.c_int, [PDEP, I32, I32, P, P, P, P, P, P]),
     "edg_fv_patch_step": (C.c_int, [PDEP, I32, I32, P, P, P, P, P, P, D, P, P]),
     "edg_fv_grid_step": (C.c_int, [PDEP, I32, I32, I32, P, P, P, P, P, D, P, P]),
+    "edg_fv_grid_step_range": (C.c_int, [PDEP, I32, I32, I32, I32, I32, P, P, P, P, P, D, P, P]),
     "edg_patch_boundary_layers": (C.c_int, [I32, I32, I32, I32, P, P, P]),
     "edg_stream_priority_range": (C.c_int, [C.POINTER(I32), C.POINTER(I32)]),
     "edg_graph_begin": (C.c_int, [P]),

@@ -490,16 +490,29 @@ int edg_fv_patch_step(const edg_pde* pde, int32_t k, int32_t npatches, const dou
 int edg_fv_grid_step(const edg_pde* pde, int32_t k, int32_t patches_per_axis, int32_t periodic,
                      const double* patch_dev, const double* dt_dev, const double* edges_dev, double* out_dev,
                      unsigned long long* dt_slots_dev, double h_cell, uint32_t* status_dev, void* stream) {
+  return edg_fv_grid_step_range(pde, k, patches_per_axis, periodic, 0, -1, patch_dev, dt_dev, edges_dev, out_dev,
+                                dt_slots_dev, h_cell, status_dev, stream);
+}
+
+int edg_fv_grid_step_range(const edg_pde* pde, int32_t k, int32_t patches_per_axis, int32_t periodic,
+                           int32_t patch_begin, int32_t patch_count, const double* patch_dev, const double* dt_dev,
+                           const double* edges_dev, double* out_dev, unsigned long long* dt_slots_dev, double h_cell,
+                           uint32_t* status_dev, void* stream) {
   unsigned long long* const trace = take_trace();   // consumed even when nothing launches
   const Unit* u = find_unit(pde);
   if (!u) return fail(EDG_ERR_CONFIG, "unsupported pde descriptor");
   if (patches_per_axis < 1) return fail(EDG_ERR_CONFIG, "empty patch grid");
   long long np = 1;
   for (int d = 0; d < pde->dim; ++d) np *= patches_per_axis;
+  if (np > 0x7fffffffLL) return fail(EDG_ERR_CONFIG, "patch grid too large");
+  if (patch_count < 0) patch_count = (int32_t)(np - patch_begin);
+  if (patch_begin < 0 || (long long)patch_begin + patch_count > np) return fail(EDG_ERR_CONFIG, "patch range outside the grid");
+  if (patch_count == 0) return EDG_OK;
   FvArgs a;
   std::memset(&a, 0, sizeof a);
   a.trace = trace;
-  a.npatches = (int32_t)np;
+  a.npatches = patch_begin + patch_count;
+  a.patch_base = patch_begin;
   a.patch = patch_dev;
   a.pgrid_n = patches_per_axis;
   a.periodic = periodic ? 1 : 0;

@@ -25,7 +25,8 @@
 namespace edg {
 
 struct FvArgs {
-  int32_t npatches;
+  int32_t npatches;        // end of the patch range (exclusive)
+  int32_t patch_base;      // first patch of the range (0: all patches)
   const double* patch;     // [B][M][k^d]
   const int32_t* nbr;      // [B][2d] or null (halos given / grid)
   int32_t pgrid_n;         // > 0: row-major pgrid_n^d patch grid, neighbours by arithmetic
@@ -372,7 +373,7 @@ template <int KIND, int DIM, int K, int MINB = FvCfg<DIM, K>::MINB>
 __global__ void __launch_bounds__(FvCfg<DIM, K>::THREADS, MINB) fv_patch_kernel(const FvArgs A) {
   const TraceScope trace_scope(A.trace);
   extern __shared__ __align__(16) double smem[];
-  fv_patch_body<KIND, DIM, K>(A, blockIdx.x, smem);
+  fv_patch_body<KIND, DIM, K>(A, A.patch_base + (int)blockIdx.x, smem);
 }
 
 template <int DIM>

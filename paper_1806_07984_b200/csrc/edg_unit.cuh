@@ -245,7 +245,7 @@ static int launch_fv_k(const FvArgs& a, cudaStream_t st) {
   const size_t smem = FvSmem<KIND, DIM, K>::BYTES;
   auto kern = fv_patch_kernel<KIND, DIM, K>;
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
-  if (a.npatches > 0) kern<<<a.npatches, FvCfg<DIM, K>::THREADS, smem, st>>>(a);
+  if (a.npatches > a.patch_base) kern<<<a.npatches - a.patch_base, FvCfg<DIM, K>::THREADS, smem, st>>>(a);
   return check_launch();
 }
 

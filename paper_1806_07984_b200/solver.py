@@ -226,6 +226,77 @@ class _Base:
         self._enqueue_step()
         self.steps_done += 1
 
+    # ------------------------------------------------- host-resident steps --
+    def _host_stream(self, q_in, q_out, bounds, order, npts, plan):
+        """One step from the host buffer q_in to the host buffer q_out,
+        streamed in slabs (cell / patch ranges `bounds`):
+
+            copy-in stream : H2D slab j          (waits for D2H slab j of the previous call)
+            current stream : dt candidates of slab j as it lands -> dt = cfl * min
+                             -> plan[i]() enqueues kernels, returns the slabs now final
+            copy-out stream: D2H of each final slab
+
+        dt is the admissible step of q_in itself (kernels.py:267-281), so the
+        result is bitwise that of set_state(q_in); step().  q_in / q_out: CPU
+        tensors of the state's shape (pinned for asynchronous copies).  q_out
+        is complete when the event `host_ready` has completed (host_wait()
+        makes the current stream wait for it); the current stream does not
+        wait, so the next call's uploads overlap this call's downloads, and
+        back-to-back calls only wait per slab for the previous call's download
+        of the same slab (other work on the state in between makes the uploads
+        wait for the current stream)."""
+        torch = self.torch
+        lib = self.lib
+        if not hasattr(self, "_sh"):
+            self._sh = {"in": torch.cuda.Stream(), "out": torch.cuda.Stream(), "prev_out": {}}
+        sh = self._sh
+        src = q_in.reshape(self.Q.shape)
+        dst = q_out.reshape(self.Q.shape)
+        main = torch.cuda.current_stream()
+        Q, Qn = self.Q, self.Qn
+        if sh.get("gen") != getattr(self, "_state_gen", 0):
+            sh["in"].wait_stream(main)
+            sh["prev_out"] = {}
+        _lib.check(lib.edg_dt_slots_reset(_lib.ptr(self.slots), _stream()), "dt reset")
+        for j in range(len(bounds) - 1):
+            c0, c1 = bounds[j], bounds[j + 1]
+            with torch.cuda.stream(sh["in"]):
+                prev = sh["prev_out"].get((c0, c1))
+                if prev is not None:
+                    sh["in"].wait_event(prev)     # host / device slab still being read by the last call's copy-out
+                Q[c0:c1].copy_(src[c0:c1], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(sh["in"])
+            main.wait_event(e)
+            _lib.check(lib.edg_cell_speed_reduce(C.byref(self.native), order, c1 - c0, npts, _lib.ptr(Q[c0:c1]),
+                                                 _lib.ptr(self.hmin), 0, _lib.ptr(self.slots), _stream()),
+                       "admissible_dt")
+        self._finalize_dt()
+        prev_out = {}
+        for run in plan:
+            for c in run():
+                c0, c1 = bounds[c], bounds[c + 1]
+                e = torch.cuda.Event()
+                e.record(main)
+                with torch.cuda.stream(sh["out"]):
+                    sh["out"].wait_event(e)
+                    dst[c0:c1].copy_(Qn[c0:c1], non_blocking=True)
+                    eo = torch.cuda.Event()
+                    eo.record(sh["out"])
+                prev_out[(c0, c1)] = eo
+        sh["prev_out"] = prev_out
+        sh["gen"] = getattr(self, "_state_gen", 0)
+        self.host_ready = torch.cuda.Event()
+        self.host_ready.record(sh["out"])
+        self.Q, self.Qn = self.Qn, self.Q
+        self.steps_done += 1
+
+    def host_wait(self):
+        """Make the current stream wait for the last step_host's downloads."""
+        ev = getattr(self, "host_ready", None)
+        if ev is not None:
+            self.torch.cuda.current_stream().wait_event(ev)
+
 
 class DGSolver(_Base):
     """ADER-DG time stepping on the GPU (Algorithm 1 semantics)."""
@@ -404,87 +475,25 @@ class DGSolver(_Base):
     def step_host(self, q_in, q_out, slabs: int = 16):
         """One step from a host state to a host buffer (the drop-in use of
         the reference's numpy API, where every call takes and returns host
-        arrays), streamed in slabs of the uniform grid so that the PCIe
-        transfers overlap each other and the kernels:
-
-            copy-in stream : H2D slab j                         (waits D2H slab j of the previous call)
-            compute stream : dt candidates of slab j (as it lands) -> dt = cfl * min
-                             -> per slab: Picard order, predictor(slab j),
-                                corrector(slab j - 1) once predictor(j) is done
-            copy-out stream: D2H slab j after its corrector
-
-        A slab is a run of whole axis-0 layers, so a cell's face neighbours
-        lie in its own or the adjacent slab; on a periodic grid slab 0 is
-        corrected last (its lower neighbour is the last slab).  dt is the
-        admissible step of q_in itself (kernels.py:267-281), reduced on the
-        device as the slabs arrive, so the result is bitwise that of
-        set_state(q_in); step().  q_in / q_out: CPU tensors of the state's
-        shape (pinned for asynchronous copies).  q_out is complete when the
-        event `host_ready` has completed (host_wait() makes the current
-        stream wait for it); the current stream itself does not wait, so the
-        next call's uploads overlap this call's downloads."""
-        torch = self.torch
+        arrays), streamed in slabs of the uniform grid (_Base._host_stream):
+        once every slab has landed and dt is reduced, the predictor of slab j
+        is followed by the corrector of slab j - 1 (its face neighbours lie in
+        slabs j - 2 .. j; on a periodic grid slab 0 is corrected last) and that
+        slab's download.  Bitwise set_state(q_in); step()."""
         if self.adaptive:
             raise ConfigError("step_host streams uniform grids only")
-        lib = self.lib
         bounds = self._slab_bounds(slabs)
-        S = len(bounds) - 1
-        if not hasattr(self, "_sh"):
-            self._sh = {"in": torch.cuda.Stream(), "out": torch.cuda.Stream(), "prev_out": {}}
-        sh = self._sh
         order = self._slab_order_buf()
-        src = q_in.reshape(self.Q.shape)
-        dst = q_out.reshape(self.Q.shape)
-        main = torch.cuda.current_stream()
         Q, Qn = self.Q, self.Qn
-        npts = self.basis.n ** self.pde.dim
-        if sh.get("gen") != getattr(self, "_state_gen", 0):
-            # other work on the state since the last step_host: the uploads
-            # wait for everything enqueued on the current stream; back-to-back
-            # calls only wait per slab for the previous call's download
-            sh["in"].wait_stream(main)
-            sh["prev_out"] = {}
-        _lib.check(lib.edg_dt_slots_reset(_lib.ptr(self.slots), _stream()), "dt reset")
-        for j in range(S):
-            c0, c1 = bounds[j], bounds[j + 1]
-            with torch.cuda.stream(sh["in"]):
-                prev = sh["prev_out"].get((c0, c1))
-                if prev is not None:
-                    sh["in"].wait_event(prev)     # host / device slab still being read by the last call's copy-out
-                Q[c0:c1].copy_(src[c0:c1], non_blocking=True)
-                e = torch.cuda.Event()
-                e.record(sh["in"])
-            main.wait_event(e)
-            _lib.check(lib.edg_cell_speed_reduce(C.byref(self.native), self.order, c1 - c0, npts, _lib.ptr(Q[c0:c1]),
-                                                 _lib.ptr(self.hmin), 0, _lib.ptr(self.slots), _stream()),
-                       "admissible_dt")
-        self._finalize_dt()
-        prev_out = {}
-        for j, ready in self._corrector_schedule(S):
-            self._slab_order_stp(Q, order, bounds[j], bounds[j + 1])
-            for c in ready:
-                c0, c1 = bounds[c], bounds[c + 1]
-                self._slab_corrector(Qn, c0, c1)
-                e = torch.cuda.Event()
-                e.record(main)
-                with torch.cuda.stream(sh["out"]):
-                    sh["out"].wait_event(e)
-                    dst[c0:c1].copy_(Qn[c0:c1], non_blocking=True)
-                    eo = torch.cuda.Event()
-                    eo.record(sh["out"])
-                prev_out[(c0, c1)] = eo
-        sh["prev_out"] = prev_out
-        sh["gen"] = getattr(self, "_state_gen", 0)
-        self.host_ready = torch.cuda.Event()
-        self.host_ready.record(sh["out"])
-        self.Q, self.Qn = self.Qn, self.Q
-        self.steps_done += 1
-
-    def host_wait(self):
-        """Make the current stream wait for the last step_host's downloads."""
-        ev = getattr(self, "host_ready", None)
-        if ev is not None:
-            self.torch.cuda.current_stream().wait_event(ev)
+        plan = []
+        for j, ready in self._corrector_schedule(len(bounds) - 1):
+            def run(j=j, ready=ready):
+                self._slab_order_stp(Q, order, bounds[j], bounds[j + 1])
+                for c in ready:
+                    self._slab_corrector(Qn, bounds[c], bounds[c + 1])
+                return ready
+            plan.append(run)
+        self._host_stream(q_in, q_out, bounds, self.order, self.basis.n ** self.pde.dim, plan)
 
     # ----------------------------------------------------------------- step --
     def _worker(self):
@@ -643,6 +652,30 @@ class FVSolver(_Base):
 
     def state(self):
         return self.Q
+
+    def step_host(self, q_in, q_out, slabs: int = 16):
+        """One step from a host state to a host buffer, streamed in slabs of
+        patch layers (_Base._host_stream): once every slab has landed and dt
+        is reduced, each slab's patch update (its halos are read from the
+        uploaded neighbour patches) is followed by that slab's download.
+        Bitwise set_state(q_in); step()."""
+        N, d = self.pmesh.N, self.pde.dim
+        S = max(1, min(int(slabs), N))
+        layer = N ** (d - 1)
+        bounds = [(N * j // S) * layer for j in range(S + 1)]
+        Q, Qn, lib = self.Q, self.Qn, self.lib
+        plan = []
+        for j in range(S):
+            def run(j=j):
+                self._trace("FVPatch")
+                _lib.check(lib.edg_fv_grid_step_range(C.byref(self.native), self.k, N, int(self.pmesh.periodic),
+                                                      bounds[j], bounds[j + 1] - bounds[j], _lib.ptr(Q),
+                                                      _lib.ptr(self.dt), _lib.ptr(self.edges), _lib.ptr(Qn),
+                                                      _lib.ptr(self.slots), self.h_cell, _lib.ptr(self.status),
+                                                      _stream()), "fv_patch_step")
+                return [j]
+            plan.append(run)
+        self._host_stream(q_in, q_out, bounds, 0, self.k ** d, plan)
 
     def _enqueue_step(self):
         lib = self.lib

@@ -92,3 +92,27 @@ def test_step_host_rejects_adaptive(edg):
     with pytest.raises(ConfigError):
         s.step_host(None, None)
 
+
+
+@pytest.mark.parametrize("cells,slabs", [(16, 1), (16, 2), (32, 3), (32, 4)])
+def test_fv_step_host_bitwise_vs_step(edg, cells, slabs):
+    """Config 4's patch update streamed from / to host buffers in slabs of
+    patch layers: bitwise the device step (which is bitwise the reference)."""
+    import torch
+    cfg = edg.configs.CONFIGS["cfg4"].with_(cells=cells)
+    P0 = edg.configs.initial_fv(cfg)
+    ref = edg.solver.FVSolver(edg.pde.euler(3), cells, 8, cfg.cfl)
+    ref.set_state(P0)
+    ref.run(3, graph=False)
+    want = ref.state().cpu().numpy()
+    s = edg.solver.FVSolver(edg.pde.euler(3), cells, 8, cfg.cfl)
+    a = torch.from_numpy(np.ascontiguousarray(P0)).pin_memory()
+    b = torch.empty_like(a).pin_memory()
+    for _ in range(3):
+        s.step_host(a, b, slabs=slabs)
+        a, b = b, a
+    s.host_wait()
+    torch.cuda.synchronize()
+    s.check_status()
+    assert np.array_equal(a.numpy(), want)
+    assert np.array_equal(s.dt_history(), ref.dt_history())
