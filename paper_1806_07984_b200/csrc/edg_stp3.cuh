@@ -44,6 +44,14 @@ namespace edg {
 #define EDG_STP3_MINB(n) ((n) <= 5 ? 2 : 1)
 #endif
 
+// axis-0 rows in the natural node order (node (i0,i1,i2) at n^2 i0 + n i1 +
+// i2: unit-stride node-phase accesses, pencil p = n i1 + i2 at p + n^2 j)
+// with the row stride padded (n = 5: 137) so the pencil phase's component
+// change inside a warp stays conflict-free; 0 = pencil-contiguous like axes 1, 2
+#ifndef EDG_STP3_A0NAT
+#define EDG_STP3_A0NAT 1
+#endif
+
 template <int KIND, int N>
 struct Stp3Cfg {
   static constexpr int M = Pde<KIND, 3>::M;
@@ -51,8 +59,10 @@ struct Stp3Cfg {
   static constexpr int NF = N * N;
   static constexpr int THREADS = ((NPC + 31) / 32) * 32;
   static constexpr int G = EDG_STP3_G(N) < N ? EDG_STP3_G(N) : N;   // time nodes per group
-  static constexpr int ROW = NPC;                             // one (axis, time node, component) row
-  static constexpr int FBUF = 3 * G * M * ROW;
+  static constexpr int ROW = NPC;                             // one (axis, time node, component) row of axes 1, 2
+  static constexpr bool A0NAT = EDG_STP3_A0NAT != 0;
+  static constexpr int ROW0 = A0NAT ? (N == 5 ? 137 : NPC + ((NPC + 1) & 1)) : NPC;   // rows of axis 0
+  static constexpr int FBUF = G * M * (ROW0 + 2 * ROW);
   static constexpr int STAGE = (1 + 3) * M * NPC;             // epilogue staging [(1+d) M][NPC]
   static constexpr int SF = FBUF > STAGE ? FBUF : STAGE;
   static constexpr int OPS = 2 * N + 2;                        // c = K^-1 lift, sum_s B[r][s]
@@ -81,14 +91,19 @@ stp_picard3_kernel(const StpArgs A) {
   const bool lane_ok = node < NPC;
   const int nd = lane_ok ? node : 0;   // idle lanes read (and never write) node 0's rows
   const int i0 = nd / NF, i1 = (nd / N) % N, i2 = nd % N;
-  // position of this node in axis a's pencil-contiguous layout
-  const int pos[DIM] = {N * (i1 * N + i2) + i0, N * (i0 * N + i2) + i1, N * (i0 * N + i1) + i2};
+  // position of this node in axis a's row layout (axes 1, 2 pencil-contiguous)
+  const int pos[DIM] = {Cf::A0NAT ? nd : N * (i1 * N + i2) + i0, N * (i0 * N + i2) + i1, N * (i0 * N + i1) + i2};
+  // row (a, g, k): axis-0 rows first (stride ROW0), then axes 1, 2 (stride ROW)
+  constexpr int ROW0 = Cf::ROW0;
+  auto row = [&](int a, int g, int k) -> int {
+    return a == 0 ? (g * M + k) * ROW0 : G * M * ROW0 + (((a - 1) * G + g) * M + k) * ROW;
+  };
   const double dt = *A.dt;
   const int nblocks = A.nwork;
   // pencil-phase map: one (component, pencil) per thread when they fill the CTA
   constexpr bool KMAP = EDG_STP3_KMAP(N) && M * NF <= THREADS && 2 * M * NF > THREADS;
   const bool pb_ok = tid < M * NF;
-  double* const pbase = sF + (pb_ok ? (tid / NF) * ROW + (tid % NF) * N : 0);
+  const int pk = pb_ok ? tid / NF : 0, pp = pb_ok ? tid % NF : 0;   // (component, pencil) of the pencil phase
 
   auto prefetch_q = [&](int b, int buf) {
     if (lane_ok && b < A.nwork) {
@@ -137,7 +152,7 @@ stp_picard3_kernel(const StpArgs A) {
 #pragma unroll
         for (int a = 0; a < DIM; ++a)
 #pragma unroll
-          for (int k = 0; k < M; ++k) sF[((a * G + g) * M + k) * ROW + pos[a]] = F[a][k];
+          for (int k = 0; k < M; ++k) sF[row(a, g, k) + pos[a]] = F[a][k];
       }
     };
     // B: in-place pencil contraction of the rows of group slots [0, ng)
@@ -151,18 +166,23 @@ stp_picard3_kernel(const StpArgs A) {
           for (int a = 0; a < DIM; ++a) {
             const double ih = sIh[a];
 #pragma unroll
+            // pencil element j: axis 0 (natural rows) at p + n^2 j, else n p + j
+            constexpr int JS0 = Cf::A0NAT ? NF : 1;
+            const int js = a == 0 ? JS0 : 1;
+            const int po = (a == 0 && Cf::A0NAT) ? pp : pp * N;
+#pragma unroll
             for (int g = 0; g < G; ++g) {
               if (g < ng) {
-                double* P = pbase + (a * G + g) * M * ROW;
+                double* P = sF + row(a, g, pk) + po;
                 double f[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) f[j] = P[j];
+                for (int j = 0; j < N; ++j) f[j] = P[j * js];
 #pragma unroll
                 for (int i = 0; i < N; ++i) {
                   double h = 0.0;
 #pragma unroll
                   for (int j = 0; j < N; ++j) h = fma(kPen[O + EDG_BASIS_D(N) + i * N + j], f[j], h);
-                  P[i] = h * ih;
+                  P[i * js] = h * ih;
                 }
               }
             }
@@ -174,17 +194,19 @@ stp_picard3_kernel(const StpArgs A) {
       for (int t = tid; t < tasks; t += THREADS) {
         const int rg = t / NF, p = t - rg * NF;          // rg = (a, g, k) within the used slots
         const int a = rg / (ng * M), rem = rg - a * ng * M;
-        double* P = sF + ((a * G) * M + rem) * ROW + p * N;
+        const bool nat = a == 0 && Cf::A0NAT;
+        const int js = nat ? NF : 1;
+        double* P = sF + row(a, rem / M, rem % M) + (nat ? p : p * N);
         double f[N];
 #pragma unroll
-        for (int j = 0; j < N; ++j) f[j] = P[j];
+        for (int j = 0; j < N; ++j) f[j] = P[j * js];
         const double ih = sIh[a];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           double h = 0.0;
 #pragma unroll
           for (int j = 0; j < N; ++j) h = fma(kPen[O + EDG_BASIS_D(N) + i * N + j], f[j], h);
-          P[i] = h * ih;
+          P[i * js] = h * ih;
         }
       }
     };
@@ -192,8 +214,7 @@ stp_picard3_kernel(const StpArgs A) {
     auto div_at = [&](int g, double (&dv)[M]) {
 #pragma unroll
       for (int k = 0; k < M; ++k)
-        dv[k] = (sF[((0 * G + g) * M + k) * ROW + pos[0]] + sF[((1 * G + g) * M + k) * ROW + pos[1]]) +
-                sF[((2 * G + g) * M + k) * ROW + pos[2]];
+        dv[k] = (sF[row(0, g, k) + pos[0]] + sF[row(1, g, k) + pos[1]]) + sF[row(2, g, k) + pos[2]];
     };
 
     int its = 0;
