@@ -51,6 +51,11 @@ namespace edg {
 #ifndef EDG_STP3_A0NAT
 #define EDG_STP3_A0NAT 1
 #endif
+// axis-1 rows likewise with i1 slowest (node at n^2 i1 + n i2 + i0, pencil
+// p = n i2 + i0 at p + n^2 j), row stride as axis 0's
+#ifndef EDG_STP3_A1NAT
+#define EDG_STP3_A1NAT 1
+#endif
 
 template <int KIND, int N>
 struct Stp3Cfg {
@@ -61,8 +66,10 @@ struct Stp3Cfg {
   static constexpr int G = EDG_STP3_G(N) < N ? EDG_STP3_G(N) : N;   // time nodes per group
   static constexpr int ROW = NPC;                             // one (axis, time node, component) row of axes 1, 2
   static constexpr bool A0NAT = EDG_STP3_A0NAT != 0;
-  static constexpr int ROW0 = A0NAT ? (N == 5 ? 137 : NPC + ((NPC + 1) & 1)) : NPC;   // rows of axis 0
-  static constexpr int FBUF = G * M * (ROW0 + 2 * ROW);
+  static constexpr bool A1NAT = A0NAT && EDG_STP3_A1NAT != 0;
+  static constexpr int ROW0 = A0NAT ? (N == 5 ? 137 : NPC + ((NPC + 1) & 1)) : NPC;   // rows of axis 0 (and 1)
+  static constexpr int ROW1 = A1NAT ? ROW0 : NPC;
+  static constexpr int FBUF = G * M * (ROW0 + ROW1 + ROW);
   static constexpr int STAGE = (1 + 3) * M * NPC;             // epilogue staging [(1+d) M][NPC]
   static constexpr int SF = FBUF > STAGE ? FBUF : STAGE;
   static constexpr int OPS = 2 * N + 2;                        // c = K^-1 lift, sum_s B[r][s]
@@ -92,12 +99,16 @@ stp_picard3_kernel(const StpArgs A) {
   const int nd = lane_ok ? node : 0;   // idle lanes read (and never write) node 0's rows
   const int i0 = nd / NF, i1 = (nd / N) % N, i2 = nd % N;
   // position of this node in axis a's row layout (axes 1, 2 pencil-contiguous)
-  const int pos[DIM] = {Cf::A0NAT ? nd : N * (i1 * N + i2) + i0, N * (i0 * N + i2) + i1, N * (i0 * N + i1) + i2};
-  // row (a, g, k): axis-0 rows first (stride ROW0), then axes 1, 2 (stride ROW)
-  constexpr int ROW0 = Cf::ROW0;
+  const int pos[DIM] = {Cf::A0NAT ? nd : N * (i1 * N + i2) + i0,
+                        Cf::A1NAT ? NF * i1 + N * i2 + i0 : N * (i0 * N + i2) + i1, N * (i0 * N + i1) + i2};
+  // row (a, g, k): axis-0 rows (stride ROW0), axis-1 rows (ROW1), axis-2 rows (ROW)
+  constexpr int ROW0 = Cf::ROW0, ROW1 = Cf::ROW1;
   auto row = [&](int a, int g, int k) -> int {
-    return a == 0 ? (g * M + k) * ROW0 : G * M * ROW0 + (((a - 1) * G + g) * M + k) * ROW;
+    return a == 0 ? (g * M + k) * ROW0
+                  : (a == 1 ? G * M * ROW0 + (g * M + k) * ROW1 : G * M * (ROW0 + ROW1) + (g * M + k) * ROW);
   };
+  // pencil layouts: axes 0 / 1 natural (pencil p at p, element stride n^2), else n p + j
+  auto nat = [&](int a) { return (a == 0 && Cf::A0NAT) || (a == 1 && Cf::A1NAT); };
   const double dt = *A.dt;
   const int nblocks = A.nwork;
   // pencil-phase map: one (component, pencil) per thread when they fill the CTA
@@ -167,9 +178,8 @@ stp_picard3_kernel(const StpArgs A) {
             const double ih = sIh[a];
 #pragma unroll
             // pencil element j: axis 0 (natural rows) at p + n^2 j, else n p + j
-            constexpr int JS0 = Cf::A0NAT ? NF : 1;
-            const int js = a == 0 ? JS0 : 1;
-            const int po = (a == 0 && Cf::A0NAT) ? pp : pp * N;
+            const int js = nat(a) ? NF : 1;
+            const int po = nat(a) ? pp : pp * N;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
               if (g < ng) {
@@ -194,9 +204,9 @@ stp_picard3_kernel(const StpArgs A) {
       for (int t = tid; t < tasks; t += THREADS) {
         const int rg = t / NF, p = t - rg * NF;          // rg = (a, g, k) within the used slots
         const int a = rg / (ng * M), rem = rg - a * ng * M;
-        const bool nat = a == 0 && Cf::A0NAT;
-        const int js = nat ? NF : 1;
-        double* P = sF + row(a, rem / M, rem % M) + (nat ? p : p * N);
+        const bool na = nat(a);
+        const int js = na ? NF : 1;
+        double* P = sF + row(a, rem / M, rem % M) + (na ? p : p * N);
         double f[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) f[j] = P[j * js];
