@@ -57,6 +57,24 @@ namespace edg {
 #define EDG_STP3_A1NAT 1
 #endif
 
+// n = 5, axis 1 (EDG_STP3_A1TAB): rows in the natural node order too (unit-
+// stride node phase) with row stride 133 (= 5 mod 16); the pencil-phase task
+// of thread t is kA1Task[t] = 25 k + 5 i0 + i2 (component k, pencil (i0, i2),
+// elements at 25 i0 + i2 + 5 j): the 125 tasks are grouped so that every
+// half-warp's 16 tasks fall on 16 distinct 8-byte bank pairs (bank =
+// (5 k + 25 i0 + i2) mod 16 has 8 or 7 tasks per bank; half-warp g takes
+// the g-th task of each bank) -- conflict-free in both phases
+#ifndef EDG_STP3_A1TAB
+#define EDG_STP3_A1TAB 1
+#endif
+static __constant__ signed char kA1Task[128] = {
+    0,   1,   2,   3,   4,   13,  14,  23,  24,  5,   6,   7,   8,   9,   18,  19,  32,  33,  10,  11,  12,  21,
+    22,  27,  28,  29,  38,  15,  16,  17,  30,  31,  40,  41,  34,  43,  20,  25,  26,  35,  36,  37,  46,  39,
+    48,  49,  54,  63,  64,  73,  42,  55,  44,  57,  58,  59,  68,  45,  50,  47,  52,  53,  62,  71,  72,  77,
+    74,  79,  56,  65,  66,  67,  80,  69,  82,  51,  60,  61,  70,  75,  76,  85,  78,  87,  88,  89,  98,  99,
+    104, 81,  90,  83,  84,  93,  94,  107, 108, 109, 86,  95,  96,  97,  102, 103, 112, 113, 114, 91,  92,  105,
+    106, 115, 116, 117, 118, 119, 100, 101, 110, 111, 120, 121, 122, 123, 124, -1,  -1,  -1};
+
 template <int KIND, int N>
 struct Stp3Cfg {
   static constexpr int M = Pde<KIND, 3>::M;
@@ -66,9 +84,10 @@ struct Stp3Cfg {
   static constexpr int G = EDG_STP3_G(N) < N ? EDG_STP3_G(N) : N;   // time nodes per group
   static constexpr int ROW = NPC;                             // one (axis, time node, component) row of axes 1, 2
   static constexpr bool A0NAT = EDG_STP3_A0NAT != 0;
-  static constexpr bool A1NAT = A0NAT && EDG_STP3_A1NAT != 0;
-  static constexpr int ROW0 = A0NAT ? (N == 5 ? 137 : NPC + ((NPC + 1) & 1)) : NPC;   // rows of axis 0 (and 1)
-  static constexpr int ROW1 = A1NAT ? ROW0 : NPC;
+  static constexpr bool A1TAB = EDG_STP3_A1TAB != 0 && N == 5 && EDG_STP3_KMAP(N) && M == 5;
+  static constexpr bool A1NAT = !A1TAB && A0NAT && EDG_STP3_A1NAT != 0;
+  static constexpr int ROW0 = A0NAT ? (N == 5 ? 137 : NPC + ((NPC + 1) & 1)) : NPC;   // rows of axis 0
+  static constexpr int ROW1 = A1TAB ? 133 : (A1NAT ? ROW0 : NPC);                   // rows of axis 1
   static constexpr int FBUF = G * M * (ROW0 + ROW1 + ROW);
   static constexpr int STAGE = (1 + 3) * M * NPC;             // epilogue staging [(1+d) M][NPC]
   static constexpr int SF = FBUF > STAGE ? FBUF : STAGE;
@@ -100,7 +119,8 @@ stp_picard3_kernel(const StpArgs A) {
   const int i0 = nd / NF, i1 = (nd / N) % N, i2 = nd % N;
   // position of this node in axis a's row layout (axes 1, 2 pencil-contiguous)
   const int pos[DIM] = {Cf::A0NAT ? nd : N * (i1 * N + i2) + i0,
-                        Cf::A1NAT ? NF * i1 + N * i2 + i0 : N * (i0 * N + i2) + i1, N * (i0 * N + i1) + i2};
+                        Cf::A1TAB ? nd : (Cf::A1NAT ? NF * i1 + N * i2 + i0 : N * (i0 * N + i2) + i1),
+                        N * (i0 * N + i1) + i2};
   // row (a, g, k): axis-0 rows (stride ROW0), axis-1 rows (ROW1), axis-2 rows (ROW)
   constexpr int ROW0 = Cf::ROW0, ROW1 = Cf::ROW1;
   auto row = [&](int a, int g, int k) -> int {
@@ -115,6 +135,10 @@ stp_picard3_kernel(const StpArgs A) {
   constexpr bool KMAP = EDG_STP3_KMAP(N) && M * NF <= THREADS && 2 * M * NF > THREADS;
   const bool pb_ok = tid < M * NF;
   const int pk = pb_ok ? tid / NF : 0, pp = pb_ok ? tid % NF : 0;   // (component, pencil) of the pencil phase
+  // axis-1 task under A1TAB: component and natural offset 25 i0 + i2 of the pencil
+  const int t1 = Cf::A1TAB ? (int)kA1Task[tid < 128 ? tid : 127] : 0;
+  const int pk1 = Cf::A1TAB ? (t1 >= 0 ? t1 / NF : 0) : pk;
+  const int po1 = Cf::A1TAB ? (t1 >= 0 ? NF * ((t1 % NF) / N) + t1 % N : 0) : 0;
 
   auto prefetch_q = [&](int b, int buf) {
     if (lane_ok && b < A.nwork) {
@@ -178,12 +202,14 @@ stp_picard3_kernel(const StpArgs A) {
             const double ih = sIh[a];
 #pragma unroll
             // pencil element j: axis 0 (natural rows) at p + n^2 j, else n p + j
-            const int js = nat(a) ? NF : 1;
-            const int po = nat(a) ? pp : pp * N;
+            const bool tab = a == 1 && Cf::A1TAB;
+            const int js = tab ? N : (nat(a) ? NF : 1);
+            const int po = tab ? po1 : (nat(a) ? pp : pp * N);
+            const int kk = tab ? pk1 : pk;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
               if (g < ng) {
-                double* P = sF + row(a, g, pk) + po;
+                double* P = sF + row(a, g, kk) + po;
                 double f[N];
 #pragma unroll
                 for (int j = 0; j < N; ++j) f[j] = P[j * js];
