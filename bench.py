@@ -179,7 +179,9 @@ def fp64_peak_tflops():
     nsm = torch.cuda.get_device_properties(0).multi_processor_count
     blocks, iters = nsm * 8, 4096
     best = 0.0
-    for _ in range(4):
+    for _ in range(6):   # clocks ramp up from idle: untimed launches first
+        _lib.check(lib.edg_probe_fp64(_lib.ptr(sink), blocks, iters, st), "probe")
+    for _ in range(8):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()

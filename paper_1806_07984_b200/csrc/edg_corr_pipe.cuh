@@ -32,11 +32,13 @@ struct CorrPipe {
 #define EDG_CORR_CPB_BIG 1
 #endif
   static constexpr int CPB = NPC >= 96 ? EDG_CORR_CPB_BIG : (EDG_CORR_PIPE_TARGET / NPC > 0 ? EDG_CORR_PIPE_TARGET / NPC : 1);
-  // EDG_CORR_WIDE (default 1): with one cell per group and more face points
-  // than nodes (3-D p = 4: 150 > 125), the CTA is sized for the face points so
-  // that the Rusanov phase is one pass over 160 threads instead of two
+  // EDG_CORR_WIDE = 1: with one cell per group and more face points than
+  // nodes (3-D p = 4: 150 > 125), the CTA is sized for the face points (one
+  // Rusanov pass over 160 threads instead of two over 128).  Off by default
+  // since q_end is loaded into registers: cfg3 1.50 ms at 128 threads against
+  // 1.61 ms at 160
 #ifndef EDG_CORR_WIDE
-#define EDG_CORR_WIDE 1
+#define EDG_CORR_WIDE 0
 #endif
   static constexpr int TOTF = 2 * DIM * NF;
   static constexpr bool WIDE = EDG_CORR_WIDE && CPB == 1 && TOTF > NPC;
