@@ -10,7 +10,6 @@
 #include "edg_faces.cuh"
 #include "edg_corr_pipe.cuh"
 #include "edg_fv.cuh"
-#include "edg_fv_sweep.cuh"
 #include "edg_dt.cuh"
 
 #define EDG_CAT2(a, b) a##b
@@ -243,12 +242,6 @@ int EDG_FN(_riemann)(int nfaces, int npts, const double* lo, const double* hi, i
 template <int K>
 static int launch_fv_k(const FvArgs& a, cudaStream_t st) {
   constexpr int KIND = EDG_UNIT_KIND, DIM = EDG_UNIT_DIM;
-  if constexpr (FvSweep<KIND, DIM, K>::ENABLED) {
-    // 3-D Euler 8^3 patches: plane sweep, every interface once (edg_fv_sweep.cuh)
-    if (a.npatches > a.patch_base)
-      fv_sweep_kernel<K, EDG_FV_SWEEP_MINB><<<a.npatches - a.patch_base, FvSweep<KIND, DIM, K>::THREADS, 0, st>>>(a);
-    return check_launch();
-  }
   const size_t smem = FvSmem<KIND, DIM, K>::BYTES;
   auto kern = fv_patch_kernel<KIND, DIM, K>;
   if (set_smem(kern, smem)) return EDG_ERR_CUDA;
