@@ -184,9 +184,9 @@ struct FastFlux<EDG_PDE_EULER, DIM> {
 
 // np.maximum semantics: NaN if either operand is NaN.
 __device__ __forceinline__ double nan_max(double a, double b) {
-  if (a != a) return a;
-  if (b != b) return b;
-  return a > b ? a : b;
+  // a NaN -> a; else b NaN -> b (a > b is false); else the larger: selects, no branches
+  const double m = a > b ? a : b;
+  return a != a ? a : m;
 }
 
 // Rusanov outcome along +axis (kernels.py:162-173), bit-exact numpy order:

@@ -294,17 +294,20 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
       for (int f2 = C::WIDE ? tid : node; f2 < TOT; f2 += C::WIDE ? THREADS : NPC) {
         const int fs = f2 / NF, f = f2 - fs * NF;
         const int a = fs >> 1, s = fs & 1;
-        double mine[M], theirs[M], out[M];
+        // face oriented along +a: lo = lower cell's (a,1) trace, hi = upper
+        // cell's (a,0).  A warp's face points span two sides, so the sides
+        // are chosen by address (one Rusanov evaluation per warp, no
+        // divergent second pass)
+        double lo[M], hi[M], out[M];
         const int b = (C::WIDE ? 0 : slot) * TRC + fs * M * NF + f;
+        const double* const plo = s == 1 ? tq : nq;
+        const double* const phi = s == 1 ? nq : tq;
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          mine[k] = tq[b + k * NF];
-          theirs[k] = nq[b + k * NF];
+          lo[k] = plo[b + k * NF];
+          hi[k] = phi[b + k * NF];
         }
-        if (s == 1)
-          rusanov<KIND, DIM>(mine, theirs, a, 1, A.pp, out);
-        else
-          rusanov<KIND, DIM>(theirs, mine, a, 1, A.pp, out);
+        rusanov<KIND, DIM>(lo, hi, a, 1, A.pp, out);
 #pragma unroll
         for (int k = 0; k < M; ++k) sJump[b + k * NF] = __dsub_rn(out[k], tf[b + k * NF]);
       }

@@ -156,10 +156,15 @@ __global__ void __launch_bounds__(CorrCfg<DIM, N>::THREADS) corrector_kernel(con
         double out[M];
         if (FUSED) {
           // face oriented along +a: lo = lower cell's (a,1) trace, hi = upper cell's (a,0)
-          if (s == 1)
-            rusanov<KIND, DIM>(mine[i], theirs[i], a, 1, A.pp, out);
-          else
-            rusanov<KIND, DIM>(theirs[i], mine[i], a, 1, A.pp, out);
+          // (sides chosen by value: a warp's face points span two sides, one
+          // Rusanov evaluation serves both instead of a divergent second pass)
+          double lo[M], hi[M];
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            lo[k] = s == 1 ? mine[i][k] : theirs[i][k];
+            hi[k] = s == 1 ? theirs[i][k] : mine[i][k];
+          }
+          rusanov<KIND, DIM>(lo, hi, a, 1, A.pp, out);
         } else {
 #pragma unroll
           for (int k = 0; k < M; ++k) out[k] = mine[i][k];
