@@ -49,14 +49,24 @@ struct FvCfg {
   // EDG_FV_Z4=1 (3-D, k = 8): a thread owns volumes z and z+4 of a row and the
   // last axis is padded to 12, which makes every warp-wide state access
   // bank-conflict-free (4 lanes per row cover 4 consecutive z, rows land in
-  // disjoint 4-bank-pair blocks); the pressure is then recomputed from the
-  // staged state instead of staged (same operations) to stay at 3 CTAs/SM
+  // disjoint 4-bank-pair blocks)
 #ifndef EDG_FV_Z4
 #define EDG_FV_Z4 1
 #endif
   static constexpr bool Z4 = EDG_FV_Z4 && DIM == 3 && K == 8;
   static constexpr int KEZ = Z4 ? 12 : ((KE % 2) ? KE : KE + 1);    // else: last axis padded to an odd length
   static constexpr int NE = ipow(KE, DIM - 1) * KEZ;    // (bank-conflict-free strided access)
+  // EDG_FV_PREC=0 (default): the pressure is staged like 1/rho and c (8 arrays
+  // per state).  Under Z4 the arrays are then spaced NE - 2 apart (the last two
+  // padding entries of the 10 x 10 x 12 block are never addressed), which is
+  // what lets three CTAs of 8 arrays share an SM: 8 * 1198 * 8 + 48 B + 1 KB
+  // reserved = 77 744 B each, 233 232 of the SM's 233 472 B.  EDG_FV_PREC=1
+  // recomputes the pressure from the staged state at every load (7 arrays)
+#ifndef EDG_FV_PREC
+#define EDG_FV_PREC 0
+#endif
+  static constexpr bool PREC = EDG_FV_PREC && Z4;
+  static constexpr int NES = (Z4 && !PREC) ? NE - 2 : NE;   // array stride
   static constexpr int NL = ipow(K, DIM - 1);           // cells per face layer
 #ifndef EDG_FV_CPT
 #define EDG_FV_CPT 2
@@ -69,9 +79,9 @@ struct FvCfg {
 template <int KIND, int DIM, int K>
 struct FvSmem {
   static constexpr int M = Pde<KIND, DIM>::M;
-  // staged parts: 1/rho, (p,) c -- under Z4 the pressure is recomputed
-  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? (FvCfg<DIM, K>::Z4 ? 2 : 3) : 0;
-  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NE * (M + NPARTS) + DIM) +
+  // staged parts: 1/rho, (p,) c -- with PREC the pressure is recomputed
+  static constexpr int NPARTS = KIND == EDG_PDE_EULER ? (FvCfg<DIM, K>::PREC ? 2 : 3) : 0;
+  static constexpr size_t BYTES = sizeof(double) * (FvCfg<DIM, K>::NES * (M + NPARTS) + DIM) +
                                   sizeof(unsigned long long) * DIM;
 };
 
@@ -81,13 +91,13 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   using P = Pde<KIND, DIM>;
   using Cf = FvCfg<DIM, K>;
   constexpr int M = P::M;
-  constexpr int NC = Cf::NC, NE = Cf::NE, NL = Cf::NL, KE = Cf::KE, KEZ = Cf::KEZ;
+  constexpr int NC = Cf::NC, NE = Cf::NES, NL = Cf::NL, KE = Cf::KE, KEZ = Cf::KEZ;   // NE: array stride
   constexpr int THREADS = Cf::THREADS, CPT = Cf::CPT;
   constexpr bool EULER = KIND == EDG_PDE_EULER;
   // ext strides: last axis 1, then KEZ, then KEZ*KE
   auto estride = [](int ax) { return ax == DIM - 1 ? 1 : (ax == DIM - 2 ? KEZ : KEZ * KE); };
 
-  constexpr bool PREC = Cf::Z4;                    // pressure recomputed from the staged state
+  constexpr bool PREC = Cf::PREC;                  // pressure recomputed from the staged state
   double* sQ = smem;                               // [M][NE]
   double* sInv = sQ + M * NE;                      // [NE] (Euler)
   constexpr bool Z4 = Cf::Z4 && CPT == 2;
