@@ -141,9 +141,9 @@ struct StpSmem {
 #define EDG_STP_T0 0
 #endif
   static constexpr bool T0 = EDG_STP_T0 && DIM == 2 && N % 2 == 0;
-  // EDG_STP_SPAD=1: per-cell flux block stride padded to 8 (mod 16) doubles
-  // so the same pencil of two cells sharing a warp lands 16 banks apart
-  // (removes the 2-way conflicts but measured no faster: off by default)
+  // EDG_STP_SPAD=1: per-cell flux block stride padded (EDG_STP_SPAD_MOD mod
+  // 16 doubles) so the same pencil of two cells sharing a warp lands on
+  // different banks (without quads measured no faster: off by default)
 #ifndef EDG_STP_SPAD
 #define EDG_STP_SPAD 0
 #endif
@@ -173,7 +173,16 @@ struct StpSmem {
   static constexpr bool BM = QUAD && EDG_STP_BM;
   static constexpr int SS0 = DIM * M * NPCP;
   static constexpr bool SPADX = (EDG_STP_SPAD || (QUAD && EDG_STP_SPAD_QUAD)) && C::CPB > 1;
-  static constexpr int SS = SPADX ? SS0 + ((8 - SS0 % 16) + 16) % 16 : SS0;
+  // cell stride mod 16 doubles.  A quad's axis-0 load asks for 2 adjacent
+  // doubles at (c/2) 4 + const, i.e. double banks {0,1}, {4,5}, {8,9} for the
+  // three quad columns of a cell; a second cell sharing the warp lands on the
+  // free banks iff its block starts at 2, 6, 10 or 14 (mod 16).  Measured on
+  // cfg2 (CFL 0.9, steps 1-10): 8 -> 0.649 ms, 2 -> 0.626, 4 -> 0.626,
+  // 14 -> 0.629; indifferent on cfg5
+#ifndef EDG_STP_SPAD_MOD
+#define EDG_STP_SPAD_MOD 2
+#endif
+  static constexpr int SS = SPADX ? SS0 + ((EDG_STP_SPAD_MOD - SS0 % 16) + 16) % 16 : SS0;
   static constexpr int FB = C::CPB * SS;                        // one flux buffer
   // time nodes per pipeline stage (one barrier per stage); EDG_STP_G overrides
 #if defined(EDG_STP_G)
