@@ -81,6 +81,42 @@ static __constant__ signed char kA1Task[128] = {
     104, 81,  90,  83,  84,  93,  94,  107, 108, 109, 86,  95,  96,  97,  102, 103, 112, 113, 114, 91,  92,  105,
     106, 115, 116, 117, 118, 119, 100, 101, 110, 111, 120, 121, 122, 123, 124, -1,  -1,  -1};
 
+
+// EDG_STP3_PLANE (n = 5, full iterations): the derivatives along axes 1 and 2
+// are contracted together by PLANE tasks -- task (g, k, i0) loads the 5 x 5
+// plane i0 of the rows F_1[g][k] and F_2[g][k] (both in natural node order,
+// 25 contiguous values each), forms
+//     H12[i1][i2] = sum_l D[i1][l] F_1[l][i2] + sum_l D[i2][l] F_2[i1][l]
+// with F_1's plane held in registers and F_2 streamed row by row, and writes
+// H12 over F_2's plane (row i1 is stored right after it was consumed).  There
+// are G M n = 125 plane tasks, one per thread; axis 0 keeps its pencil tasks.
+// Shared-memory accesses per node and (time node, component): flux stores 3,
+// plane 2 + 1, axis-0 pencils 1 + 1, derivative loads 2 = 10 instead of the
+// pencil formulation's 12 -- the kernel is bound by shared-memory wavefronts
+// (DESIGN.md section 4).  Both rows then use the stride n^3 = 125 (= 13 mod
+// 16, a task's base lands on bank pair (13 (5 g + k) + 9 i0) mod 16, at most 8
+// tasks per pair); kPlaneTask assigns the tasks to lanes so that the 16 tasks
+// of every half-warp sit on 16 distinct bank pairs, and kA1Task125 does the
+// same for the axis-1 pencil tasks of the reduced first iteration (task
+// 25 k + 5 i0 + i2 at bank pair (13 k + 9 i0 + i2) mod 16).
+#ifndef EDG_STP3_PLANE
+#define EDG_STP3_PLANE 1
+#endif
+static __constant__ signed char kPlaneTask[128] = {
+    124, 38, 84, 41, 50, 43, 119, 21, 74, 16, 24, 113, 51, 45, 14, 79, 4, 121, 82, 7, 101, 22, 96, 33, 10,
+    35, 11, 104, 76, 93, 110, 47, 36, 39, 105, 86, 85, 81, 59, 66, 19, 64, 88, 42, 44, 78, 61, 31, 20, 9, 6,
+    5, 65, 103, 107, 18, 122, 80, 56, 28, 67, 46, 109, 95, 73, 52, 123, 87, 118, 117, 90, 99, 1, 112, 2, 40,
+    92, 94, 111, 13, 25, 68, 71, 53, 58, 70, 27, 34, 0, 115, 49, 12, 120, 30, 29, 63, 23, 37, 116, 54, 91,
+    106, 114, 89, 3, 48, 60, 8, 97, 77, 62, 15, 69, 75, 98, 55, 26, 100, 83, 57, 32, 102, 108, 72, 17, -1,
+    -1, -1};
+static __constant__ signed char kA1Task125[128] = {
+    124, 38, 84, 41, 50, 45, 43, 36, 14, 119, 24, 105, 35, 93, 59, 18, 4, 121, 82, 7, 16, 39, 22, 9, 86, 73,
+    104, 107, 64, 21, 103, 70, 74, 20, 113, 79, 110, 78, 96, 61, 81, 11, 19, 68, 80, 101, 31, 54, 85, 51, 46,
+    6, 94, 109, 52, 47, 25, 71, 76, 116, 56, 65, 23, 106, 33, 10, 30, 123, 88, 42, 117, 53, 28, 99, 112, 91,
+    92, 67, 13, 98, 5, 66, 87, 118, 122, 37, 44, 27, 40, 89, 0, 55, 12, 111, 49, 62, 90, 58, 95, 1, 69, 34,
+    115, 3, 100, 60, 120, 97, 108, 75, 26, 57, 2, 29, 114, 77, 48, 83, 63, 15, 32, 8, 102, 72, 17, -1, -1,
+    -1};
+
 template <int KIND, int N>
 struct Stp3Cfg {
   static constexpr int M = Pde<KIND, 3>::M;
@@ -93,7 +129,9 @@ struct Stp3Cfg {
   static constexpr bool A1TAB = EDG_STP3_A1TAB != 0 && N == 5 && EDG_STP3_KMAP(N) && M == 5;
   static constexpr bool A1NAT = !A1TAB && A0NAT && EDG_STP3_A1NAT != 0;
   static constexpr int ROW0 = A0NAT ? (N == 5 ? 137 : NPC + ((NPC + 1) & 1)) : NPC;   // rows of axis 0
-  static constexpr int ROW1 = A1TAB ? 133 : (A1NAT ? ROW0 : NPC);                   // rows of axis 1
+  // plane tasks for axes 1 + 2 in full iterations (see kPlaneTask)
+  static constexpr bool PLANE = EDG_STP3_PLANE != 0 && A1TAB && G == N && M == N && A0NAT;
+  static constexpr int ROW1 = A1TAB ? (PLANE ? NPC : 133) : (A1NAT ? ROW0 : NPC);   // rows of axis 1
   static constexpr int FBUF = G * M * (ROW0 + ROW1 + ROW);
   static constexpr int STAGE = (1 + 3) * M * NPC;             // epilogue staging [(1+d) M][NPC]
   static constexpr int SF = FBUF > STAGE ? FBUF : STAGE;
@@ -142,7 +180,10 @@ stp_picard3_kernel(const StpArgs A) {
   const bool pb_ok = tid < M * NF;
   const int pk = pb_ok ? tid / NF : 0, pp = pb_ok ? tid % NF : 0;   // (component, pencil) of the pencil phase
   // axis-1 task under A1TAB: component and natural offset 25 i0 + i2 of the pencil
-  const int t1 = Cf::A1TAB ? (int)kA1Task[tid < 128 ? tid : 127] : 0;
+  const int t1 = Cf::A1TAB ? (int)(Cf::PLANE ? kA1Task125 : kA1Task)[tid < 128 ? tid : 127] : 0;
+  // plane task (g, k, i0) of this thread: row r = g M + k, plane i0
+  const int tpl = Cf::PLANE ? (int)kPlaneTask[tid < 128 ? tid : 127] : -1;
+  const int pl_r = tpl >= 0 ? tpl / N : 0, pl_p = tpl >= 0 ? tpl % N : 0;
   const int pk1 = Cf::A1TAB ? (t1 >= 0 ? t1 / NF : 0) : pk;
   const int po1 = Cf::A1TAB ? (t1 >= 0 ? NF * ((t1 % NF) / N) + t1 % N : 0) : 0;
 
@@ -204,6 +245,65 @@ stp_picard3_kernel(const StpArgs A) {
     };
     // B: in-place pencil contraction of the rows of group slots [0, ng)
     auto pencils = [&](int ng) {
+      if constexpr (Cf::PLANE) {
+        if (ng == G) {
+          auto run = [&](auto scaled) {
+            constexpr bool SC = decltype(scaled)::value;
+            // axis 0: the thread's (component, pencil) in every time node's row
+            if (pb_ok) {
+              const double ih = SC ? sIh[0] : 1.0;
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                double* P = sF + row(0, g, pk) + pp;
+                double f[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) f[j] = P[j * NF];
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                  double h = 0.0;
+#pragma unroll
+                  for (int j = 0; j < N; ++j) h = fma(kPen[O + EDG_BASIS_D(N) + i * N + j], f[j], h);
+                  P[i * NF] = SC ? h * ih : h;
+                }
+              }
+            }
+            // axes 1 + 2: one plane task
+            if (tpl >= 0) {
+              const double ih1 = SC ? sIh[1] : 1.0, ih2 = SC ? sIh[2] : 1.0;
+              const double* P1 = sF + G * M * ROW0 + pl_r * ROW1 + NF * pl_p;
+              double* P2 = sF + G * M * (ROW0 + ROW1) + pl_r * ROW + NF * pl_p;
+              double f1[N][N];
+#pragma unroll
+              for (int l = 0; l < N; ++l)
+#pragma unroll
+                for (int j = 0; j < N; ++j) f1[l][j] = P1[l * N + j];
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                double f2[N], o[N];
+#pragma unroll
+                for (int l = 0; l < N; ++l) f2[l] = P2[i * N + l];
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                  double h1 = 0.0, h2 = 0.0;
+#pragma unroll
+                  for (int l = 0; l < N; ++l) {
+                    h1 = fma(kPen[O + EDG_BASIS_D(N) + i * N + l], f1[l][j], h1);
+                    h2 = fma(kPen[O + EDG_BASIS_D(N) + j * N + l], f2[l], h2);
+                  }
+                  o[j] = SC ? fma(h1, ih1, h2 * ih2) : h1 + h2;
+                }
+#pragma unroll
+                for (int j = 0; j < N; ++j) P2[i * N + j] = o[j];
+              }
+            }
+          };
+          if (iso)
+            run(std::false_type{});
+          else
+            run(std::true_type{});
+          return;
+        }
+      }
       if constexpr (KMAP) {
         // thread (component k, pencil p): every row (a, g, k) of its k at its
         // pencil -- no index arithmetic, and the warp-wide stride-n accesses
@@ -265,7 +365,13 @@ stp_picard3_kernel(const StpArgs A) {
       }
     };
     // C: divergence of group slot g at this node
-    auto div_at = [&](int g, double (&dv)[M]) {
+    auto div_at = [&](int g, double (&dv)[M], bool plane = false) {
+      if (Cf::PLANE && plane) {
+        // axis 0 + the plane tasks' sum of axes 1 and 2 (left in axis 2's rows)
+#pragma unroll
+        for (int k = 0; k < M; ++k) dv[k] = sF[row(0, g, k) + pos[0]] + sF[row(2, g, k) + pos[2]];
+        return;
+      }
 #pragma unroll
       for (int k = 0; k < M; ++k)
         dv[k] = (sF[row(0, g, k) + pos[0]] + sF[row(1, g, k) + pos[1]]) + sF[row(2, g, k) + pos[2]];
@@ -312,12 +418,6 @@ stp_picard3_kernel(const StpArgs A) {
     // full iteration: qn = c q + sum_s B[r][s] div F(qc_s); returns "not converged"
     auto body = [&](const double (&qc)[N][M], double (&qn)[N][M], int it) -> bool {
 #pragma unroll
-      for (int k = 0; k < M; ++k) {
-        const double q0 = lane_ok ? q0s[k * NPC] : 1.0;
-#pragma unroll
-        for (int r = 0; r < N; ++r) qn[r][k] = kPen[O + EDG_BASIS_KLIFT(N) + r] * q0;
-      }
-#pragma unroll
       for (int s0 = 0; s0 < N; s0 += G) {
         const int ng = (N - s0) < G ? (N - s0) : G;
 #pragma unroll
@@ -331,11 +431,21 @@ stp_picard3_kernel(const StpArgs A) {
         __syncthreads();
         pencils(ng);
         __syncthreads();
+        if (s0 == 0) {
+          // the new iterate starts from the lift of the initial state (set
+          // here, after the pencil / plane phase, so it is not live across it)
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const double q0 = lane_ok ? q0s[k * NPC] : 1.0;
+#pragma unroll
+            for (int r = 0; r < N; ++r) qn[r][k] = kPen[O + EDG_BASIS_KLIFT(N) + r] * q0;
+          }
+        }
 #pragma unroll
         for (int g = 0; g < G; ++g)
           if (g < ng) {
             double dv[M];
-            div_at(g, dv);
+            div_at(g, dv, ng == G);
             const double sc = -(dt * kPen[O + EDG_BASIS_W(N) + s0 + g]) * ihs;   // (-dt) w_s (/ h when iso)
 #pragma unroll
             for (int r = 0; r < N; ++r) {
