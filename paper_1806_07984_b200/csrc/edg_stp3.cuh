@@ -159,7 +159,10 @@ stp_picard3_kernel(const StpArgs A) {
   const int tid = threadIdx.x;
   const int node = tid;
   const bool lane_ok = node < NPC;
-  const int nd = lane_ok ? node : 0;   // idle lanes read (and never write) node 0's rows
+  // idle lanes read (and never write) the last node's rows: the same address
+  // as lane NPC - 1 of their warp (a broadcast; node 0's address shared a bank
+  // with the warp's first lane and cost an extra wavefront per load)
+  const int nd = lane_ok ? node : NPC - 1;
   const int i0 = nd / NF, i1 = (nd / N) % N, i2 = nd % N;
   // position of this node in axis a's row layout (axes 1, 2 pencil-contiguous)
   const int pos[DIM] = {Cf::A0NAT ? nd : N * (i1 * N + i2) + i0,
