@@ -6,6 +6,7 @@
 
 #include "edg_stp.cuh"
 #include "edg_stp3.cuh"
+#include "edg_stp2.cuh"
 #include "edg_stp_ck.cuh"
 #include "edg_faces.cuh"
 #include "edg_corr_pipe.cuh"
@@ -113,6 +114,11 @@ static int launch_stp_n(const StpArgs& a, cudaStream_t st) {
     // 3-D, one cell per CTA: the pencil formulation (edg_stp3.cuh)
     using C3 = Stp3Cfg<KIND, N>;
     return launch_stp_grid(stp_picard3_kernel<KIND, N>, C3::THREADS, C3::BYTES, a.nwork, a, st);
+  } else if constexpr (DIM == 2 && Stp2Cfg<KIND, N>::ENABLED) {
+    // 2-D Euler, n = 4: the plane formulation (edg_stp2.cuh)
+    using C2 = Stp2Cfg<KIND, N>;
+    return launch_stp_grid(stp_picard2_kernel<KIND, N>, C2::THREADS, C2::BYTES, (a.nwork + C2::CPB - 1) / C2::CPB, a,
+                           st);
   } else {
     using Cf = StpCfg<DIM, N>;
     return launch_stp_grid(stp_picard_kernel<KIND, DIM, N>, Cf::THREADS, StpSmem<KIND, DIM, N>::BYTES,
