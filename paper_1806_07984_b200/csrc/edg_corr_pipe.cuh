@@ -60,7 +60,14 @@ struct CorrPipe {
   static constexpr int STAGE = QE + NB * TB;
   static constexpr int NV = GRID ? 2 * DIM * N : CPB * 2 * DIM * N;    // lift vectors (per cell when adaptive)
   // resident CTAs asked of ptxas: 5 fit the shared memory of the unstaged-q_end 3-D kernel
-  static constexpr int MINB = (QEG && DIM == 3) ? 5 : 1;
+  // 2-D: four CTAs per SM (64 registers) -- with ptxas's free choice (96
+  // registers, 2 CTAs) the CTAs spun on the stage mbarrier (ncu: 40 % of the
+  // samples on the wait loop's branch); cfg2 corrector 82.7 -> 66.0 (3) ->
+  // 63.7 us (4)
+#ifndef EDG_CORR_MINB_2D
+#define EDG_CORR_MINB_2D 4
+#endif
+  static constexpr int MINB = (QEG && DIM == 3) ? 5 : (DIM == 2 ? EDG_CORR_MINB_2D : 1);
   static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TB + NV) +
                                   sizeof(unsigned long long) * (1 + CPB + CPB + 2) +
                                   sizeof(unsigned) * (((2 * DIM * CPB + 1) & ~1));
