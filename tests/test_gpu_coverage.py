@@ -56,6 +56,39 @@ def test_every_instantiation_matches_oracle(edg, name, dim, p):
         assert rel_linf(tf[:, j], ref["trace_f"][k]) < 1e-12
 
 
+@pytest.mark.parametrize("dim,p,edges,C", [(2, 3, (1 / 27, 1 / 19), 7), (2, 3, (1 / 27, 1 / 27), 9),
+                                           (3, 4, (1 / 16, 1 / 12, 1 / 20), 3), (2, 5, (1 / 27, 1 / 19), 4)])
+def test_plane_predictors_anisotropic_ragged_mixed_convergence(edg, dim, p, edges, C):
+    """The plane-task predictors (edg_stp2.cuh for 2-D n = 4, edg_stp3.cuh's
+    plane tasks for 3-D n = 5) on anisotropic cells (1/h applied per axis
+    inside the task instead of folded into the time coefficients), with a
+    cell count that leaves the last CTA's work block ragged, and with cells
+    of one block converging after different iteration counts (a smooth cell,
+    a rough one): iteration counts equal the oracle's, values to 1e-12."""
+    import torch
+    from oracle import batched, ops
+    rng = np.random.default_rng(7 * p + dim)
+    Q = _states(rng, "euler", dim, p + 1, C)
+    Q[0] = Q[0].mean(axis=tuple(range(1, dim + 1)), keepdims=True)      # constant cell: converges at once
+    Q[-1, 0] *= 1.0 + 0.3 * rng.random(Q[-1, 0].shape)                    # rough cell: more iterations
+    dt = 0.2 * min(edges) / ((2 * p + 1) * 2.5)
+    ref = batched.predictor_picard_b(Q, ops.euler(dim), dt, ops.basis_for(p), edges)
+    out = edg.kernels.stp_picard_batch(torch.from_numpy(Q).cuda(), edg.pde.euler(dim), dt, edg.basis.get_basis(p),
+                                       edges)
+    torch.cuda.synchronize()
+    its = out["iterations"].cpu().numpy()
+    assert np.array_equal(its, ref["iterations"])
+    assert len(set(its.tolist())) > 1, "the cells were meant to converge at different iterations"
+    assert np.array_equal(out["converged"].cpu().numpy().astype(bool), ref["converged"])
+    assert rel_linf(out["q_end"].cpu().numpy(), ref["q_end"]) < 1e-12
+    assert rel_linf(out["q_int"].cpu().numpy(), ref["q_int"]) < 1e-12
+    keys = [(a, s) for a in range(dim) for s in (0, 1)]
+    tq, tf = out["trace_q"].cpu().numpy(), out["trace_f"].cpu().numpy()
+    for j, k in enumerate(keys):
+        assert rel_linf(tq[:, j], ref["trace_q"][k]) < 1e-12
+        assert rel_linf(tf[:, j], ref["trace_f"][k]) < 1e-12
+
+
 @pytest.mark.parametrize("p", [6, 7])
 def test_3d_high_order_steps_vs_oracle(edg, p):
     """3-D Euler at the paper's highest orders (Table 1 measures p = 7,
