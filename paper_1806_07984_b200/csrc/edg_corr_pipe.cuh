@@ -67,7 +67,10 @@ struct CorrPipe {
 #ifndef EDG_CORR_MINB_2D
 #define EDG_CORR_MINB_2D 4
 #endif
-  static constexpr int MINB = (QEG && DIM == 3) ? 5 : (DIM == 2 ? EDG_CORR_MINB_2D : 1);
+#ifndef EDG_CORR_MINB_3D
+#define EDG_CORR_MINB_3D 5
+#endif
+  static constexpr int MINB = (QEG && DIM == 3) ? EDG_CORR_MINB_3D : (DIM == 2 ? EDG_CORR_MINB_2D : 1);
   static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TB + NV) +
                                   sizeof(unsigned long long) * (1 + CPB + CPB + 2) +
                                   sizeof(unsigned) * (((2 * DIM * CPB + 1) & ~1));
@@ -139,6 +142,20 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
   // The three contiguous blocks go through the bulk-copy (TMA) engine when
   // 16-byte aligned and sized (one instruction each, completion counted on
   // the stage's mbarrier); otherwise cooperative cp.async.
+  // L2 priorities (EDG_CORR_L2HINT): q_end and trace_f are read once
+  // (evict_first), the own trace_q block is read again by the 2d neighbours
+  // -- the i0 neighbours a whole plane of cells later (evict_last), so that
+  // re-read finds it in L2 instead of DRAM
+#ifndef EDG_CORR_L2HINT
+#define EDG_CORR_L2HINT 1
+#endif
+  const unsigned long long pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
+  auto bulk_copy = [&](int i, void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    if (EDG_CORR_L2HINT && GRID)
+      bulk_g2s_hint(dst, src, bytes, bar, i == 1 ? pol_last : pol_first);
+    else
+      bulk_g2s(dst, src, bytes, bar);
+  };
   auto load_group = [&](int g, double* st, unsigned long long* bar) {
     const int c0 = A.cell_base + g * CPB;
     const int nc = min(CPB, A.ncells - c0);
@@ -170,7 +187,7 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
         __syncthreads();
         if (tid == 0) {
 #pragma unroll
-          for (int i = B0; i < NBK; ++i) bulk_g2s(dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
+          for (int i = B0; i < NBK; ++i) bulk_copy(i, dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
         }
         double* nq = st + C::QE + (C::NB - 1) * C::TB;
         for (int bi = tid; bi < nc * 2 * DIM; bi += THREADS) {
@@ -194,7 +211,7 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
       mbar_arrive_expect_tx(bar, bulk_bytes);
 #pragma unroll
       for (int i = B0; i < NBK; ++i)
-        if (bulk[i]) bulk_g2s(dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
+        if (bulk[i]) bulk_copy(i, dsts[i], srcs[i], (unsigned)cnt[i] * 8u, bar);
     }
 #pragma unroll
     for (int i = B0; i < NBK; ++i)
@@ -270,7 +287,10 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
     double qeg[M];
     if constexpr (C::QEG) {
 #pragma unroll
-      for (int k = 0; k < M; ++k) qeg[k] = has_cell ? __ldg(A.q_end + (size_t)cell * M * NPC + (size_t)k * NPC + node) : 0.0;
+      for (int k = 0; k < M; ++k)
+        qeg[k] = has_cell ? (EDG_CORR_L2HINT ? __ldcs(A.q_end + (size_t)cell * M * NPC + (size_t)k * NPC + node)
+                                             : __ldg(A.q_end + (size_t)cell * M * NPC + (size_t)k * NPC + node))
+                          : 0.0;
     }
     const double* tq = cur + C::QE;
     const double* tf = cur + C::QE + (GRID ? C::TB : 0);
@@ -339,7 +359,10 @@ corrector_grid_pipe_kernel(const CorrArgs A) {
       double* qo = A.q_out + (size_t)cell * M * NPC + node;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        qo[(size_t)k * NPC] = qn[k];
+        if (EDG_CORR_L2HINT && GRID)
+          __stcs(qo + (size_t)k * NPC, qn[k]);
+        else
+          qo[(size_t)k * NPC] = qn[k];
         finite = finite && (fabs(qn[k]) <= 1.7976931348623157e308);
       }
     }
