@@ -179,9 +179,17 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   constexpr int NHT = (2 * DIM * NL + THREADS - 1) / THREADS;
   double qi_[NIT][M], qh_[NHT][M];
   int xh_[NHT];
+  // interior volume staged by (thread, u): under Z4 the volumes the thread
+  // later owns (row tid / 4, z = tid % 4 and z + 4) -- a warp's stores then
+  // cover 8 rows x 4 z like its state loads (conflict-free; the linear
+  // assignment put rows 12 apart on overlapping banks: 4.1 wavefronts per
+  // STS.64 instead of 2), and every 32-byte sector of a load is still used
+  // by 4 lanes -- else tid + u * THREADS
+  constexpr bool ZST = Cf::Z4 && CPT == 2 && NIT == 2;
+  auto stage_cell = [&](int u) { return ZST ? (tid / (K / 2)) * K + tid % (K / 2) + u * (K / 2) : tid + u * THREADS; };
 #pragma unroll
   for (int u = 0; u < NIT; ++u) {
-    const int c = tid + u * THREADS;
+    const int c = stage_cell(u);
 #pragma unroll
     for (int k = 0; k < M; ++k) qi_[u][k] = c < NC ? __ldg(src + k * NC + c) : 0.0;
   }
@@ -234,7 +242,7 @@ __device__ __forceinline__ void fv_patch_body(const FvArgs& A, const int b, doub
   }
 #pragma unroll
   for (int u = 0; u < NIT; ++u)
-    if (tid + u * THREADS < NC) stage(ext_of_cell(tid + u * THREADS), qi_[u]);
+    if (stage_cell(u) < NC) stage(ext_of_cell(stage_cell(u)), qi_[u]);
 #pragma unroll
   for (int u = 0; u < NHT; ++u)
     if (xh_[u] >= 0) stage(xh_[u], qh_[u]);

@@ -466,13 +466,31 @@ stp_picard3_kernel(const StpArgs A) {
         for (int k = 0; k < M; ++k) below = below & (fabs(qn[r][k] - qc[r][k]) < A.tol);
       return finish(it, below);   // the barrier also guards the rows for the next iteration
     };
-    for (int it = 2; any && it <= max_iter;) {
-      any = body(acc, qh, it);
-      inacc = false;
-      if (!any || ++it > max_iter) break;
-      any = body(qh, acc, it);
-      inacc = true;
-      ++it;
+    // EDG_STP3_PP = 1: the loop is unrolled by two so that qh and acc swap roles
+    // (no copies, but two copies of the iteration body in the instruction
+    // stream); 0: one body, the new iterate copied back
+#ifndef EDG_STP3_PP
+#define EDG_STP3_PP 1
+#endif
+    if constexpr (EDG_STP3_PP != 0) {
+      for (int it = 2; any && it <= max_iter;) {
+        any = body(acc, qh, it);
+        inacc = false;
+        if (!any || ++it > max_iter) break;
+        any = body(qh, acc, it);
+        inacc = true;
+        ++it;
+      }
+    } else {
+#pragma unroll 1
+      for (int it = 2; any && it <= max_iter; ++it) {
+        any = body(acc, qh, it);
+        inacc = false;
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int k = 0; k < M; ++k) acc[r][k] = qh[r][k];
+      }
     }
     if (inacc) {
 #pragma unroll
