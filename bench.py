@@ -507,7 +507,7 @@ def measure_device(cfg, steps, warmup, ws, dist, dev, peak64, local):
                                       "peak": hbm, "frac": cb / hbm if hbm else None}
         # uniform: dt finalize, STP, corrector, 3 ordering kernels; adaptive
         # (cfg5): dt finalize, 2 STP, 2 face solves, restriction, corrector
-        launches = steps * (7 if cfg.kind == "dg-amr" else 6)
+        launches = steps * (7 if cfg.kind == "dg-amr" else (6 if ncells >= 8192 else 3))
         roof = dict(kernels["stp_picard"], kernel="stp_picard")
     # share of the eager step's GPU time (same pass as the kernel events, spins removed)
     ms_busy = ms_eager - gate_total_ms

@@ -314,6 +314,12 @@ class _Base:
 class DGSolver(_Base):
     """ADER-DG time stepping on the GPU (Algorithm 1 semantics)."""
 
+    # the predictor's work order (cells sorted by their last Picard count so
+    # that CTAs are homogeneous) only matters once the cells outnumber the
+    # resident predictor slots; below this the three ordering launches cost
+    # more than they save (config 1: 729 cells, 19 us per step, 6 launches)
+    ORDER_MIN_CELLS = 8192
+
     def __init__(self, pde: PdeDescriptor, order: int, mesh, cfl: float, tol: float = 1e-10, max_iter=None,
                  check_finite: bool = True, max_steps: int = 4096, two_streams: bool = True):
         torch = self.torch = _torch()
@@ -574,8 +580,10 @@ class DGSolver(_Base):
                                               _stream()), "corrector")
             if tm:
                 tm.end("corrector")
-            _lib.check(lib.edg_order_by_iterations(self.ncells, _lib.ptr(self.iterations), _lib.ptr(self.work_order),
-                                                   _lib.ptr(self.order_scratch), _stream()), "order")
+            if self.ncells >= self.ORDER_MIN_CELLS:
+                _lib.check(lib.edg_order_by_iterations(self.ncells, _lib.ptr(self.iterations),
+                                                       _lib.ptr(self.work_order), _lib.ptr(self.order_scratch),
+                                                       _stream()), "order")
         else:
             nsk, F = self.nface_sk, self.mesh.nleaf
 
