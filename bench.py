@@ -676,6 +676,55 @@ def measure_secondary(ws, dist, dev, peak64, local):
     return out
 
 
+def pcie_probe(host_a, host_b):
+    """This box's host<->device copy rates on the e2e buffers (pinned, up to
+    256 MB): H2D alone, D2H alone, and both at once on two streams (GB/s per
+    direction) -- the ceiling of the end-to-end number, which moves the whole
+    state both ways every step."""
+    import torch
+    n = min(host_a.numel(), 32 << 20)
+    a, b = host_a.reshape(-1)[:n], host_b.reshape(-1)[:n]
+    d1 = torch.empty(n, dtype=host_a.dtype, device="cuda")
+    d2 = torch.empty(n, dtype=host_a.dtype, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    nbytes = n * host_a.element_size()
+
+    def timed(fn, reps=3):
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            s1.synchronize()
+            s2.synchronize()
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        return nbytes / (best * 1e-3) / 1e9
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            d1.copy_(a, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            b.copy_(d2, non_blocking=True)
+
+    def both():
+        h2d()
+        d2h()
+
+    saved = b.clone()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    out = {"h2d": timed(h2d), "d2h": timed(d2h), "duplex_per_direction": timed(both), "bytes": nbytes}
+    b.copy_(saved)
+    torch.cuda.synchronize()
+    return out
+
+
 def measure_e2e(solver, Q0, dof, steps, ws, dist, dev, slabs=None):
     """Public API with host buffers: every step uploads the state from pinned
     host memory (set_state), advances one step, downloads the result."""
@@ -712,11 +761,14 @@ def measure_e2e(solver, Q0, dof, steps, ws, dist, dev, slabs=None):
     b.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(dist, a.elapsed_time(b), dev)
+    pcie = pcie_probe(host, out)
     api = (f"{type(solver).__name__}.step_host(pinned host in, pinned host out): slab-streamed H2D / kernels / D2H, "
            "dt from the uploaded state" if streamed else
            "set_state(pinned host) + step() + copy to pinned host")
     return {"value": dof * steps * ws / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nb,
-            "d2h_bytes_per_step": nb, "ms_per_step": ms / steps, "api": api}
+            "d2h_bytes_per_step": nb, "ms_per_step": ms / steps, "api": api, "pcie_gbs": pcie,
+            "pcie_floor_ms_per_step": (nb / (pcie["duplex_per_direction"] * 1e9) * 1e3
+                                       if pcie and pcie.get("duplex_per_direction") else None)}
 
 
 def main():
