@@ -9,3 +9,4 @@ timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${T}_pytest_gpu.log 2
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/${T}_smoke.log
 bash tools/gpu_bench_all.sh ${T}
 bash tools/gpu_ncu_set.sh ${T}
+# afterwards, here: bash tools/collect_evidence.sh ${T}  (copies the run into profiles/round2/)
