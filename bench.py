@@ -42,7 +42,7 @@ from paper_1806_07984_b200 import configs as cf  # noqa: E402
 from paper_1806_07984_b200 import costs  # noqa: E402
 
 METRIC = "DoF-updates/s per time step on 1 B200; % of FP64/HBM roofline per kernel"
-EAGER_GATE_US = 1000     # GPU spin ahead of each eager (kernel-event) step, see run_ours
+EAGER_GATE_US = 3000     # GPU spin ahead of each eager (kernel-event) step, see run_ours
 UNIT = "DoF-updates/s"
 
 
@@ -422,7 +422,7 @@ def measure_device(cfg, steps, warmup, ws, dist, dev, peak64, local):
 
     # pass 1 (eager launches, CUDA events around every hot kernel on the
     # launching stream): the roofline numerators
-    # Each eager step starts behind a ~1 ms GPU spin (torch.cuda._sleep) so
+    # Each eager step starts behind a ~3 ms GPU spin (torch.cuda._sleep) so
     # that the host has enqueued the whole step before its first kernel runs:
     # otherwise, on the small configurations (cfg1, cfg5: tens of us per step)
     # the per-kernel event pairs would include host launch gaps.  The spin is
