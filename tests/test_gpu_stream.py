@@ -28,8 +28,11 @@ def _initial(edg, cfg, N):
     return edg.configs.initial_dg_uniform(c)
 
 
+# slabs = None: the slab count step_host picks from the state size (one slab
+# for these small states; cfg3 at 24^3 is 69 MB -> 16 slabs)
 @pytest.mark.parametrize("tag,N,slabs", [("cfg2", 12, 1), ("cfg2", 12, 5), ("cfg2", 12, 12), ("cfg3", 8, 3),
-                                         ("cfg3", 8, 8), ("cfg1", 27, 16)])
+                                         ("cfg3", 8, 8), ("cfg1", 27, 16), ("cfg1", 27, None), ("cfg2", 12, None),
+                                         ("cfg3", 24, None)])
 def test_step_host_bitwise_vs_step(edg, tag, N, slabs):
     import torch
     cfg = edg.configs.CONFIGS[tag]
