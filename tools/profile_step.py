@@ -22,8 +22,12 @@ def main():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--cells", type=int, default=None)
+    ap.add_argument("--lib", default=None, help="variant build of libenclavedg_b200.so")
     a = ap.parse_args()
     import torch
+    if a.lib:
+        from paper_1806_07984_b200 import _lib
+        _lib.load(a.lib)
     cfg = cf.CONFIGS[a.config]
     if a.cells:
         cfg = cfg.with_(cells=a.cells)
